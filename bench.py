@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the FV hot path (BASELINE.json metric: fp64 cell-updates/s and
+% of HBM roofline at 1/2/4/8 B200).
+
+Workload (config.workload): BASELINE configs[2] -- 2-D Euler, 16384 x 16384
+cells, Lax-Liu configuration 3 (synthetic, seeded/analytic), periodic, the
+paper's constant dt checked every step, y-slabs over N GPUs
+(strong scaling).  A "step" is one pass of the whole hot path: CFL reduction
+(fused check), x/y Lax-Friedrichs fluxes, conservative update (+ halo exchange
+and max-all-reduce for N > 1).  The state (2 x 8.6 GB) is far larger than L2,
+so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 cell-updates/sec and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "cell-updates/s"
+GAMMA = 1.4
+CFL = 0.45
+BYTES_PER_CELL = {"euler": 64, "advection": 16, "spray": 96}   # algorithmic: read W^n + write W^{n+1}
+
+WORKLOADS = {
+    # name: (system, nx, ny, description)
+    "c3_euler_16384": ("euler", 16384, 16384, "BASELINE configs[2]: 2D Euler nVar=4, 16384x16384, Lax-Liu 3, "
+                                              "periodic, fixed dt checked each step, y-slabs (strong scaling)"),
+    "c2_euler_1024": ("euler", 1024, 1024, "BASELINE configs[1]: 2D Euler nVar=4, 1024x1024, Lax-Liu 3"),
+    "c5_euler_8192_per_gpu": ("euler", 8192, 8192, "BASELINE configs[4]: 8192^2 cells per GPU (weak scaling)"),
+}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_key):
+    """dram bytes per launch of the step kernel from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gen_ic(system, nx, ny, rows):
+    """Lax-Liu 3 in row chunks (bounded temporaries) into one AoS array."""
+    from paper_1701_05431_b200 import inputs
+    j0, j1 = rows
+    out = np.empty((j1 - j0, nx, 4))
+    for a in range(j0, j1, 1024):
+        b = min(j1, a + 1024)
+        out[a - j0:b - j0] = inputs.euler_lax_liu3(nx, ny, rows=(a, b), gamma=GAMMA)
+    return out
+
+
+def cpu_baseline(nx, ny, budget_s=12.0):
+    """The oracle as it stands (single-threaded C, -O2 -ffp-contract=off) on a
+    bounded sample: full-width row bands of the same workload, periodic."""
+    import oracle as O
+    from paper_1701_05431_b200 import inputs
+    rows = min(ny, 256)
+    band = inputs.euler_lax_liu3(nx, ny, rows=(ny // 2 - rows // 2, ny // 2 + rows // 2), gamma=GAMMA)
+    cfg = O.Config(nx=nx, ny=rows, system=O.EULER, param=(GAMMA,), y1=rows / ny)
+    dt = CFL * (1.0 / nx) / 2.5
+    t0 = time.perf_counter()
+    steps = 0
+    W = band
+    while True:
+        W = O.transport_step(cfg, W, dt)
+        steps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return {"value": nx * rows * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} transport steps on a {nx}x{rows} full-width row band of the workload "
+                      f"(periodic band), {el:.1f} s, 1 thread"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    system, nx, ny, desc = WORKLOADS[args.workload]
+    import oracle as O
+    from paper_1701_05431_b200 import inputs
+    # size the band so that warmup + steps take ~60 s of CPU at ~10 M cell-updates/s
+    total = max(1, args.steps + args.warmup)
+    rows = int(max(2, min(ny, 60e6 / total / nx)))
+    band = inputs.euler_lax_liu3(nx, ny, rows=(ny // 2 - rows // 2, ny // 2 - rows // 2 + rows), gamma=GAMMA)
+    cfg = O.Config(nx=nx, ny=rows, system=O.EULER, param=(GAMMA,), y1=rows / ny)
+    dt = CFL * (1.0 / nx) / 2.5
+    W = band
+    for _ in range(args.warmup):
+        W = O.transport_step(cfg, W, dt)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        W = O.transport_step(cfg, W, dt)
+    el = time.perf_counter() - t0
+    val = nx * rows * args.steps / el
+    sample = f"each step = one oracle transport step on a {nx}x{rows} full-width row band of the workload"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload, "description": desc, "nx": nx, "ny": ny,
+                                        "sample_rows": rows},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3_euler_16384", choices=sorted(WORKLOADS))
+    ap.add_argument("--naive", action="store_true", help="paper's one-thread-per-cell kernel (baseline)")
+    ap.add_argument("--adaptive", action="store_true", help="adaptive dt (smax reduced in the epilogue)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1701_05431_b200 import fv2d
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    system, nx, ny_global, desc = WORKLOADS[args.workload]
+    weak = args.workload.startswith("c5")
+    ny = ny_global * world if weak else ny_global
+    if ny % world:
+        raise SystemExit(f"ny={ny} not divisible by {world}")
+    H = ny // world
+    nccl_id = None
+    if world > 1:
+        obj = [fv2d.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    flags = fv2d.FLAG_NAIVE if args.naive else 0
+    s = fv2d.Solver(nx, ny, fv2d.EULER, param=(GAMMA,), rank=rank, nranks=world, device=local, flags=flags,
+                    nccl_id=nccl_id, stream=stream.cuda_stream)
+    W0 = gen_ic(system, nx, ny, (rank * H, (rank + 1) * H))
+    s.set_state(W0)
+    dt, smax0 = s.compute_dt(CFL)    # the paper's constant dt, set at start
+
+    def steps(k):
+        if args.adaptive:
+            s.step_adaptive(CFL, k, log=False)
+        else:
+            s.step(dt, k)
+
+    steps(args.warmup)
+    s.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed
+    st0 = s.stats()
+    s.set_profiling(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        steps(args.steps)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    st1 = s.stats()
+    s.set_profiling(False)
+    s.synchronize()                      # no latched CFL/non-finite error in the timed steps
+    kern_ms = st1["step_kernel_ms"] / max(1, st1["step_kernels_timed"])
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+    t = torch.tensor([ms, kern_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, kern_max = float(t[0]), float(t[1])
+    cells_total = nx * ny
+    value = cells_total * args.steps / (ms_max * 1e-3)
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        hostbuf = torch.empty(W0.size, dtype=torch.float64, pin_memory=True)
+        hostbuf.numpy()[:] = W0.ravel()
+        ptr = hostbuf.data_ptr()
+        s.set_state_ptr(ptr)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            s.set_state_ptr(ptr)          # H2D of this step's input (pinned) + layout conversion
+            s.step(dt, 1)
+            s.get_state_ptr(ptr)          # D2H of the step's result
+        e1.record(stream)
+        barrier()
+        et = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        nbytes = W0.size * 8
+        e2e = {"value": cells_total * args.e2e_steps / (float(et[0]) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
+               "api": "fv2d_set_state(host AoS, pinned) + fv2d_step + fv2d_get_state(host AoS)"}
+        del hostbuf
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(nx, ny)
+
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        bpc = BYTES_PER_CELL[system]
+        cells_per_launch = nx * H
+        achieved = bpc * cells_per_launch / (kern_max * 1e-3) / 1e9
+        kernel = "fv_step_naive_kernel<Euler>" if args.naive else "fv_step_kernel<Euler,4,64>"
+        traffic = ncu_traffic(kernel)
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "description": desc, "nx": nx, "ny": ny,
+                       "rows_per_gpu": H, "mode": "adaptive dt" if args.adaptive else "fixed dt (checked)",
+                       "dt": dt, "kernel": kernel,
+                       "parallelism": f"y-slabs x{world}",
+                       "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % (nx * H * 32 / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_cell": bpc, "kernel_ms": kern_max, "cells_per_launch": cells_per_launch},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

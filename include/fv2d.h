@@ -1,0 +1,191 @@
+/*
+ * fv2d.h -- C ABI of libfv2d.so, the B200 (sm_100a) hot path of the first-order
+ * finite-volume scheme of arXiv:1701.05431 (Essadki et al., "A task-driven
+ * implementation of a simple numerical solver for hyperbolic conservation laws").
+ *
+ * Problem statement followed by this interface (PAPER.md = P:, SPEC.md = S:):
+ *   dW/dt + div F(W) = S(W), W in R^nVar                      (eq:conservation_law)
+ *   Nx x Ny Cartesian cells on [x0,x1] x [y0,y1]
+ *   W* = W - dt/dx (F~_{i+1/2} - F~_{i-1/2}) - dt/dy (...)    (eq:VF_scheme)
+ *   F~ = Lax-Friedrichs with directional sigma
+ *   dt * max |lambda| <= min(dx, dy), fixed dt checked         (eq:CFL_cond)
+ *   W^{n+1} = W* + dt S(W*)                                   (eq:SourceTerm)
+ * Systems: scalar advection (nVar 1, BASELINE configs[0]), Euler (nVar 4,
+ * eq:Euler P:626-636, S = 0), evaporating spray (nVar 6, eq:Essadki P:938-999,
+ * source with the NDF reconstruction of S:401-419).  Arithmetic is IEEE
+ * binary64 in the canonical evaluation order of DESIGN.md §3.1 with no FMA
+ * contraction, so transport results are bitwise those of a plain CPU loop.
+ *
+ * Conventions
+ *  - Every call returns an fv2d_status; nothing throws, nothing aborts.
+ *  - A context is thread-compatible, not thread-safe: one thread at a time.
+ *  - Host arrays are owned by the caller; the library copies in/out.  Device
+ *    buffers, the NCCL communicator and device scalars are owned by the context.
+ *  - Stepping is asynchronous on the context's CUDA stream.  Numerical errors
+ *    (CFL violation, non-admissible state, reconstruction failure) are latched
+ *    on the device; once latched every later step is a no-op and the readable
+ *    state is W^k of the failing step k (ping-pong buffers are never half
+ *    written).  They are reported by fv2d_synchronize / fv2d_get_state /
+ *    fv2d_compute_dt and described by fv2d_last_error.
+ *  - Layouts: FV2D_AOS is the paper's Cell array: double
+ *    W[ny][nx][nvar] (x fastest, variable innermost).  FV2D_SOA is
+ *    double W[nvar][ny][nx].  With nranks > 1 every host array holds this
+ *    rank's slab only: rows [rank*ny/nranks, (rank+1)*ny/nranks).
+ */
+#ifndef FV2D_H
+#define FV2D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FV2D_VERSION_MAJOR 1
+#define FV2D_VERSION_MINOR 0
+
+typedef enum {
+  FV2D_OK = 0,
+  FV2D_E_ARG = 1,       /* invalid argument / configuration (usage error, S:612 code 1) */
+  FV2D_E_CFL = 2,       /* fixed dt violates eq:CFL_cond at the start of a step */
+  FV2D_E_NONFINITE = 3, /* non-admissible or non-finite state (rho<=0, p<=0, NaN, inf) */
+  FV2D_E_RECON = 4,     /* spray NDF reconstruction failed to converge */
+  FV2D_E_CUDA = 5,      /* CUDA runtime error (message in fv2d_last_error) */
+  FV2D_E_NCCL = 6,      /* NCCL error */
+  FV2D_E_STATE = 7      /* call not valid in the context's current state (e.g. no state set) */
+} fv2d_status;
+
+typedef enum { FV2D_ADVECTION = 0, FV2D_EULER = 1, FV2D_SPRAY = 2 } fv2d_system;
+
+/* Boundary conditions per axis.  Periodic is the paper's domain (R/Z)^2.
+ * Dirichlet: the ghost cell is the constant state cfg.dirichlet.
+ * Wall: the ghost is the mirror of the boundary cell with the normal momentum
+ * negated (Euler, spray); not defined for advection (FV2D_E_ARG). */
+typedef enum { FV2D_BC_PERIODIC = 0, FV2D_BC_DIRICHLET = 1, FV2D_BC_WALL = 2 } fv2d_bc;
+
+typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
+
+/* Kernel / schedule options (cfg.flags). */
+#define FV2D_FLAG_NAIVE 0x1u        /* paper's GPU mapping: one thread per cell,
+                                        every neighbour re-derived, every face computed twice.
+                                        Same bits, ~2.5x the FP64 work; kept as a baseline. */
+#define FV2D_FLAG_SPLIT_SOURCE 0x2u /* spray: source as a separate pass after transport
+                                        (default: fused into the transport pass, same math) */
+
+typedef struct {
+  int32_t nx, ny;          /* global mesh, >= 1; ny % (nranks*nslabs) == 0 */
+  int32_t nvar;            /* must equal the system's nVar (1, 4, 6) */
+  int32_t system;          /* fv2d_system */
+  int32_t bc_x, bc_y;      /* fv2d_bc */
+  double x0, x1, y0, y1;   /* domain; dx = (x1-x0)/nx, dy = (y1-y0)/ny */
+  double param[8];         /* advection: a_x, a_y | euler: gamma | spray: K, theta */
+  double dirichlet[6];     /* constant ghost state for FV2D_BC_DIRICHLET */
+  int32_t rank, nranks;    /* y-slab decomposition across processes (1 GPU each) */
+  int32_t nslabs;          /* y-slabs per process on the same device (>= 1); their
+                              ghost rows are exchanged exactly like the ranks' */
+  int32_t device;          /* CUDA device ordinal */
+  uint32_t flags;          /* FV2D_FLAG_* */
+  int32_t reserved[7];     /* must be 0 */
+} fv2d_config;
+
+typedef struct fv2d_ctx fv2d_ctx;
+
+typedef struct {
+  int64_t steps;           /* steps issued (including no-op steps after a latched error) */
+  int64_t kernel_launches; /* kernels launched by this context so far */
+  int64_t newton_iters;    /* spray: Newton iterations summed over cells and steps, if counted */
+  double dt;               /* current device dt (adaptive mode), 0 if unset */
+  double step_kernel_ms;   /* with profiling on: summed device time of the step kernels
+                              (CUDA events recorded on the context stream around each
+                              step-kernel launch), since profiling was enabled */
+  int64_t step_kernels_timed; /* number of step-kernel launches in step_kernel_ms */
+} fv2d_stats;
+
+/* Library version; never fails. */
+fv2d_status fv2d_version(int32_t* major, int32_t* minor);
+
+/* Default-initialised config: periodic unit square, Euler gamma = 1.4, 1 rank, 1 slab. */
+fv2d_status fv2d_config_default(fv2d_config* cfg, int32_t nx, int32_t ny, int32_t system);
+
+/* NCCL unique id for nranks > 1 (call on rank 0, broadcast the 128 bytes, e.g.
+ * with torch.distributed).  FV2D_E_NCCL if libnccl.so.2 cannot be loaded. */
+fv2d_status fv2d_nccl_unique_id(uint8_t id[128]);
+
+/* Create a context: validates cfg, selects cfg.device, allocates the two
+ * ping-pong SoA buffers of this rank's slab(s) (plus ghost rows and a staging
+ * buffer), and for nranks > 1 initialises an NCCL communicator from nccl_id
+ * (collective over all ranks).  cuda_stream: a cudaStream_t to run on (NULL =
+ * the legacy default stream); it must outlive the context. */
+fv2d_status fv2d_create(const fv2d_config* cfg, const uint8_t* nccl_id, void* cuda_stream,
+                        fv2d_ctx** out);
+
+/* Release every resource of ctx (NULL is accepted). */
+fv2d_status fv2d_destroy(fv2d_ctx* ctx);
+
+/* Initial condition W^0: copy this rank's slab from a host array in
+ * `layout`, fill the ghost rows (halo exchange for nranks > 1), reset the step
+ * counter, the latched error and the adaptive dt.  Synchronous. */
+fv2d_status fv2d_set_state(fv2d_ctx* ctx, const double* host, fv2d_layout layout);
+
+/* Same from a device array (SoA [nvar][ny_local][nx], tight pitch); asynchronous. */
+fv2d_status fv2d_set_state_device(fv2d_ctx* ctx, const double* dev, fv2d_layout layout);
+
+/* Copy the current state W^k of this rank's slab to a host array.  Synchronous.
+ * Returns the latched error, if any (the copied state is then W^k of the
+ * failing step). */
+fv2d_status fv2d_get_state(fv2d_ctx* ctx, double* host, fv2d_layout layout);
+
+/* CFL reduction (eq:CFL_cond): smax = max over all cells (all ranks) of
+ * max(|lambda|_x, |lambda|_y) of the current state; dt = (cfl*min(dx,dy))/smax.
+ * Also installs dt as the adaptive time step.  Synchronous.  smax/dt may be NULL. */
+fv2d_status fv2d_compute_dt(fv2d_ctx* ctx, double cfl, double* dt, double* smax);
+
+/* Check a fixed dt against eq:CFL_cond on the current state without stepping:
+ * FV2D_E_CFL if dt*smax > min(dx,dy).  Synchronous.  smax may be NULL. */
+fv2d_status fv2d_check_dt(fv2d_ctx* ctx, double dt, double* smax);
+
+/* nsteps steps with the paper's constant dt: each step checks
+ * dt*smax(W^n) <= min(dx,dy) (fused into the step pass) and computes W^{n+1}
+ * = transport (eq:VF_scheme) + source (eq:SourceTerm, spray only).  On a CFL
+ * violation at step k the error is latched and the state stays W^k.
+ * Asynchronous (no host synchronisation).  FV2D_E_ARG if dt <= 0 or nsteps < 0. */
+fv2d_status fv2d_step(fv2d_ctx* ctx, double dt, int32_t nsteps);
+
+/* nsteps steps with dt_n = (cfl*min(dx,dy))/smax(W^n) (BASELINE north_star
+ * "CFL time-step reduction"); smax(W^{n+1}) is reduced in the epilogue of step
+ * n.  dt_log (nsteps doubles, may be NULL) receives every dt used; passing a
+ * non-NULL dt_log synchronises.  FV2D_E_ARG if cfl <= 0 or cfl > 1. */
+fv2d_status fv2d_step_adaptive(fv2d_ctx* ctx, double cfl, int32_t nsteps, double* dt_log);
+
+/* One standalone splitting step W <- W + dt S(W) (eq:SourceTerm) on the
+ * current state; identity for S = 0 systems.  Asynchronous. */
+fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt);
+
+/* Wait for all work of ctx; return the latched numerical error, if any. */
+fv2d_status fv2d_synchronize(fv2d_ctx* ctx);
+
+/* Zero-copy view of the current device state of local slab `slab`:
+ * element (v, j, i) is at d_ptr[v*plane_stride + j*pitch + i], j in [0, ny_slab).
+ * Valid until the next step. */
+fv2d_status fv2d_device_state(fv2d_ctx* ctx, int32_t slab, double** d_ptr, int64_t* pitch,
+                              int64_t* plane_stride, int32_t* ny_slab);
+
+/* Description of the last error: message (NUL-terminated, truncated to n), the
+ * step index, the global cell index j*nx+i (lowest index among offending cells)
+ * and the offending value (speed for E_CFL).  Any output pointer may be NULL. */
+fv2d_status fv2d_last_error(fv2d_ctx* ctx, char* buf, size_t n, int64_t* step, int64_t* cell,
+                            double* value);
+
+/* Counters; with profiling on, synchronises and folds the pending kernel events
+ * into step_kernel_ms. */
+fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out);
+
+/* enable != 0: record a CUDA event pair around every step-kernel launch (for the
+ * roofline measurement of the dominant kernel); resets the accumulated time. */
+fv2d_status fv2d_set_profiling(fv2d_ctx* ctx, int32_t enable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FV2D_H */

@@ -1,0 +1,947 @@
+// fv2d_api.cu -- host side of libfv2d: the C ABI of include/fv2d.h.
+//
+// Owns the device state (two ping-pong SoA buffers per slab, packed ghost
+// rows, device scalars), launches the sm_100a kernels of fv2d_kernels.cuh on
+// the caller's stream, and drives the NCCL halo exchange / max-all-reduce for
+// nranks > 1 (libnccl.so.2 is loaded at run time with dlopen, so a process
+// that already holds torch's NCCL shares that one copy).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "fv2d.h"
+#include "fv2d_kernels.cuh"
+
+using namespace fv2d;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.loaded) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+#define SYM(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name))
+  SYM(GetUniqueId, "ncclGetUniqueId");
+  SYM(CommInitRank, "ncclCommInitRank");
+  SYM(CommDestroy, "ncclCommDestroy");
+  SYM(GroupStart, "ncclGroupStart");
+  SYM(GroupEnd, "ncclGroupEnd");
+  SYM(Send, "ncclSend");
+  SYM(Recv, "ncclRecv");
+  SYM(AllReduce, "ncclAllReduce");
+  SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+  g_nccl.loaded = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.GroupStart &&
+                  g_nccl.GroupEnd && g_nccl.Send && g_nccl.Recv && g_nccl.AllReduce;
+  return g_nccl.loaded;
+}
+
+// ------------------------------------------------------------------ GL-24 table
+// Gauss-Legendre nodes/weights on [0,1] by Newton's method on P_24 in long
+// double; uploaded once to constant memory.
+void gl24_table(double t[24], double wt[24][8]) {
+  const int n = 24;
+  for (int k = 0; k < n; ++k) {
+    long double x = cosl(3.14159265358979323846264338327950288L * (k + 0.75L) / (n + 0.5L));
+    long double dp = 0;
+    for (int it = 0; it < 200; ++it) {
+      long double p0 = 1, p1 = x;
+      for (int l = 2; l <= n; ++l) {
+        long double p2 = ((2 * l - 1) * x * p1 - (l - 1) * p0) / l;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1);
+      long double d = p1 / dp;
+      x -= d;
+      if (fabsl(d) < 1e-21L) break;
+    }
+    long double p0 = 1, p1 = x;
+    for (int l = 2; l <= n; ++l) {
+      long double p2 = ((2 * l - 1) * x * p1 - (l - 1) * p0) / l;
+      p0 = p1;
+      p1 = p2;
+    }
+    dp = n * (x * p1 - p0) / (x * x - 1);
+    const long double w = 2 / ((1 - x * x) * dp * dp);
+    const int q = n - 1 - k;  // ascending t
+    t[q] = (double)((x + 1) / 2);
+    const double wq = (double)(w / 2);
+    double tp = 1.0;
+    for (int m = 0; m < 8; ++m) {
+      wt[q][m] = wq * tp;
+      tp = tp * t[q];
+    }
+  }
+}
+
+int nvar_of(int system) {
+  switch (system) {
+    case FV2D_ADVECTION: return 1;
+    case FV2D_EULER: return 4;
+    case FV2D_SPRAY: return 6;
+    default: return -1;
+  }
+}
+
+constexpr int kWarps = 4;
+constexpr int kRows = 64;
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct fv2d_ctx {
+  fv2d_config cfg{};
+  cudaStream_t stream = nullptr;
+  int nv = 0, nx = 0, H = 0, pitch = 0, nslabs = 1, G = 1;
+  long long plane = 0;
+  double dx = 0, dy = 0, hmin = 0;
+  // per local slab
+  double* buf[kMaxSlabs][2] = {};
+  double* gs[kMaxSlabs][2] = {};
+  double* gn[kMaxSlabs][2] = {};
+  double* send_s = nullptr;  // nranks > 1: packed boundary rows to send
+  double* send_n = nullptr;
+  double* staging = nullptr;
+  size_t staging_bytes = 0;
+  // device scalars
+  unsigned long long* dscal = nullptr;  // [0]=smax [1]=pending [2]=status [3]=bad_cell [4..5]=reduced
+  unsigned int* done = nullptr;
+  double* dt_dev = nullptr;
+  double* dt_log = nullptr;
+  long long dt_log_cap = 0;
+  unsigned long long* newton = nullptr;
+  double* trig = nullptr;  // sx[nx] cx[nx] sy[ny] cy[ny]
+  ncclComm_t comm = nullptr;
+  // host state
+  bool has_state = false;
+  bool dt_valid = false;
+  long long steps = 0;
+  long long launches = 0;
+  // profiling: event pairs around step-kernel launches
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  double prof_ms = 0.0;
+  long long prof_n = 0;
+  std::string err;
+  long long err_step = -1, err_cell = -1;
+  double err_value = NAN;
+};
+
+namespace {
+
+fv2d_status set_err(fv2d_ctx* c, fv2d_status st, const char* fmt, ...) {
+  if (c) {
+    char b[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(b, sizeof b, fmt, ap);
+    va_end(ap);
+    c->err = b;
+  }
+  return st;
+}
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return set_err(ctx, FV2D_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));            \
+  } while (0)
+
+#define CKN(call)                                                                                  \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess)                                                                         \
+      return set_err(ctx, FV2D_E_NCCL, "%s failed: %s", #call,                                     \
+                     g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "?");                     \
+  } while (0)
+
+#define CKL()                                                                                      \
+  do {                                                                                             \
+    ++ctx->launches;                                                                               \
+    cudaError_t e_ = cudaGetLastError();                                                           \
+    if (e_ != cudaSuccess) return set_err(ctx, FV2D_E_CUDA, "launch failed: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+// Ghost targets of local slab s for writes landing in ghost buffers of parity q.
+void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
+  const int g = ctx->cfg.rank * ctx->nslabs + s;
+  const int G = ctx->G;
+  const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
+  const int my_y = nvar_of(ctx->cfg.system) == 4 ? 2 : (nvar_of(ctx->cfg.system) == 6 ? 5 : -1);
+  d.dst_s = nullptr;
+  d.dst_n = nullptr;
+  d.mirror_s = -1;
+  d.mirror_n = -1;
+  // south boundary row (row 0) -> south neighbour's north ghost
+  if (g > 0 || per) {
+    const int gs_ = (g - 1 + G) % G;
+    if (gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ctx->gn[gs_ % ctx->nslabs][q];
+    else d.dst_s = ctx->send_s;
+  } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
+    d.dst_s = ctx->gs[s][q];
+    d.mirror_s = my_y;
+  }
+  // north boundary row (row H-1) -> north neighbour's south ghost
+  if (g < G - 1 || per) {
+    const int gn_ = (g + 1) % G;
+    if (gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ctx->gs[gn_ % ctx->nslabs][q];
+    else d.dst_n = ctx->send_n;
+  } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
+    d.dst_n = ctx->gn[s][q];
+    d.mirror_n = my_y;
+  }
+}
+
+// Arguments of a pass reading parity p (and writing parity 1-p).
+StepArgs make_args(const fv2d_ctx* ctx, int p) {
+  StepArgs a;
+  memset(&a, 0, sizeof a);
+  const int q = 1 - p;
+  a.nslabs = ctx->nslabs;
+  for (int s = 0; s < ctx->nslabs; ++s) {
+    SlabDesc& d = a.slab[s];
+    d.in = ctx->buf[s][p];
+    d.out = ctx->buf[s][q];
+    d.gs = ctx->gs[s][p];
+    d.gn = ctx->gn[s][p];
+    ghost_targets(ctx, s, q, d);
+    d.row0 = (ctx->cfg.rank * ctx->nslabs + s) * ctx->H;
+    d.H = ctx->H;
+  }
+  a.nx = ctx->nx;
+  a.pitch = ctx->pitch;
+  a.plane = ctx->plane;
+  a.bcx = ctx->cfg.bc_x;
+  for (int v = 0; v < kMaxVar; ++v) a.dirx[v] = ctx->cfg.dirichlet[v];
+  a.dx = ctx->dx;
+  a.dy = ctx->dy;
+  a.hmin = ctx->hmin;
+  switch (ctx->cfg.system) {
+    case FV2D_ADVECTION: a.sys[0] = ctx->cfg.param[0]; a.sys[1] = ctx->cfg.param[1]; break;
+    case FV2D_EULER: a.sys[0] = ctx->cfg.param[0]; a.sys[1] = ctx->cfg.param[0] - 1.0; break;
+    case FV2D_SPRAY: a.sys[0] = ctx->cfg.param[0]; a.sys[1] = ctx->cfg.param[1]; break;
+  }
+  a.dt_dev = ctx->dt_dev;
+  a.dt_log = ctx->dt_log;
+  a.smax_slot = ctx->dscal + 0;
+  a.pending = ctx->dscal + 1;
+  a.status = ctx->dscal + 2;
+  a.bad_cell = ctx->dscal + 3;
+  a.done = ctx->done;
+  a.fused_finalize = ctx->cfg.nranks == 1 ? 1 : 0;
+  a.fuse_source = (ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_SPLIT_SOURCE)) ? 1 : 0;
+  if (ctx->trig) {
+    a.sx_tab = ctx->trig;
+    a.cx_tab = ctx->trig + ctx->nx;
+    a.sy_tab = ctx->trig + 2 * ctx->nx;
+    a.cy_tab = ctx->trig + 2 * ctx->nx + ctx->cfg.ny;
+  }
+  a.newton_iters = ctx->newton;
+  return a;
+}
+
+// Kernel dispatch on the system.
+template <template <class> class K, class... Args>
+void dispatch(int system, Args&&... args) {
+  switch (system) {
+    case FV2D_ADVECTION: K<Advection>::run(args...); break;
+    case FV2D_EULER: K<Euler>::run(args...); break;
+    case FV2D_SPRAY: K<Spray>::run(args...); break;
+  }
+}
+
+template <class Sys>
+struct LaunchStep {
+  static void run(const fv2d_ctx* ctx, const StepArgs& a) {
+    if (ctx->cfg.flags & FV2D_FLAG_NAIVE) {
+      dim3 grid((ctx->nx + 31) / 32, (ctx->H + 7) / 8, ctx->nslabs);
+      fv_step_naive_kernel<Sys><<<grid, 256, 0, ctx->stream>>>(a);
+    } else {
+      const int cols = 30 * kWarps;
+      dim3 grid((ctx->nx + cols - 1) / cols, (ctx->H + kRows - 1) / kRows, ctx->nslabs);
+      fv_step_kernel<Sys, kWarps, kRows><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+    }
+  }
+};
+
+template <class Sys>
+struct LaunchReduce {
+  static void run(const fv2d_ctx* ctx, const StepArgs& a) {
+    const long long n = (long long)ctx->nx * ctx->H;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+    reduce_smax_kernel<Sys><<<dim3(blocks, 1, ctx->nslabs), 256, 0, ctx->stream>>>(a);
+  }
+};
+
+template <class Sys>
+struct LaunchArgmax {
+  static void run(const fv2d_ctx* ctx, const StepArgs& a, double smax, unsigned long long* out) {
+    const long long n = (long long)ctx->nx * ctx->H;
+    int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+    argmax_kernel<Sys><<<dim3(blocks, 1, ctx->nslabs), 256, 0, ctx->stream>>>(a, smax, out);
+  }
+};
+
+int cur_parity(const fv2d_ctx* ctx) { return (int)(ctx->steps & 1); }
+
+// NCCL halo exchange into ghost buffers of parity q, from send_s/send_n.
+fv2d_status exchange(fv2d_ctx* ctx, int q) {
+  if (ctx->cfg.nranks == 1) return FV2D_OK;
+  const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
+  const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
+  const bool has_s = r > 0 || per, has_n = r < P - 1 || per;
+  const size_t cnt = (size_t)ctx->nv * ctx->pitch;
+  CKN(g_nccl.GroupStart());
+  if (has_s) CKN(g_nccl.Send(ctx->send_s, cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, ctx->stream));
+  if (has_n) CKN(g_nccl.Recv(ctx->gn[0][q], cnt, ncclFloat64, (r + 1) % P, ctx->comm, ctx->stream));
+  if (has_n) CKN(g_nccl.Send(ctx->send_n, cnt, ncclFloat64, (r + 1) % P, ctx->comm, ctx->stream));
+  if (has_s) CKN(g_nccl.Recv(ctx->gs[0][q], cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, ctx->stream));
+  CKN(g_nccl.GroupEnd());
+  return FV2D_OK;
+}
+
+// max-all-reduce of [smax bits, pending status] into dscal[4..5].
+fv2d_status allreduce_scalars(fv2d_ctx* ctx) {
+  CKN(g_nccl.AllReduce(ctx->dscal + 0, ctx->dscal + 4, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+  return FV2D_OK;
+}
+
+fv2d_status ensure_dt_log(fv2d_ctx* ctx, long long need) {
+  if (need <= ctx->dt_log_cap) return FV2D_OK;
+  long long cap = std::max<long long>(need, std::max<long long>(1024, 2 * ctx->dt_log_cap));
+  double* nb = nullptr;
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMalloc(&nb, cap * sizeof(double)));
+  CK(cudaMemset(nb, 0, cap * sizeof(double)));
+  if (ctx->dt_log) {
+    CK(cudaMemcpy(nb, ctx->dt_log, ctx->dt_log_cap * sizeof(double), cudaMemcpyDeviceToDevice));
+    CK(cudaFree(ctx->dt_log));
+  }
+  ctx->dt_log = nb;
+  ctx->dt_log_cap = cap;
+  return FV2D_OK;
+}
+
+fv2d_status read_status(fv2d_ctx* ctx, unsigned long long* st_out) {
+  unsigned long long st = 0;
+  CK(cudaMemcpyAsync(&st, ctx->dscal + 2, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *st_out = st;
+  return FV2D_OK;
+}
+
+// Translate a latched status word into an error code + description.
+fv2d_status report(fv2d_ctx* ctx, unsigned long long st);
+
+// Smax of the current state over all slabs/ranks -> dscal[0] (or [4] after all-reduce).
+fv2d_status reduce_current(fv2d_ctx* ctx, double* smax_out, unsigned long long* pending_out) {
+  StepArgs a = make_args(ctx, cur_parity(ctx));
+  CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  dispatch<LaunchReduce>(ctx->cfg.system, ctx, a);
+  CKL();
+  unsigned long long h[2];
+  if (ctx->cfg.nranks > 1) {
+    fv2d_status s = allreduce_scalars(ctx);
+    if (s) return s;
+    CK(cudaMemcpyAsync(h, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    CK(cudaMemcpyAsync(h, ctx->dscal + 0, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double s;
+  memcpy(&s, &h[0], sizeof s);
+  *smax_out = s;
+  *pending_out = h[1];
+  return FV2D_OK;
+}
+
+fv2d_status report(fv2d_ctx* ctx, unsigned long long st) {
+  if (st == 0) return FV2D_OK;
+  const int code = (int)(st >> 56);
+  const long long step = (long long)(st & 0x00FFFFFFFFFFFFFFull);
+  ctx->err_step = step;
+  unsigned long long bc = ~0ull;
+  cudaMemcpy(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost);
+  ctx->err_cell = bc == ~0ull ? -1 : (long long)bc;
+  switch (code) {
+    case ST_CFL:
+      return set_err(ctx, FV2D_E_CFL, "CFL violated at the start of step %lld: dt*smax > min(dx,dy) (cell %lld)",
+                     step, ctx->err_cell);
+    case ST_NONFINITE:
+      return set_err(ctx, FV2D_E_NONFINITE, "non-admissible state W^%lld (cell %lld)", step, ctx->err_cell);
+    case ST_RECON:
+      return set_err(ctx, FV2D_E_RECON, "NDF reconstruction failed in step %lld (cell %lld)", step, ctx->err_cell);
+    default:
+      return set_err(ctx, FV2D_E_STATE, "unknown latched status %llx", st);
+  }
+}
+
+// Locate the diagnostic cell of a latched error on the state W^k.
+fv2d_status diagnose(fv2d_ctx* ctx, unsigned long long st) {
+  const int code = (int)(st >> 56);
+  const long long step = (long long)(st & 0x00FFFFFFFFFFFFFFull);
+  const int p = (int)(step & 1);
+  StepArgs a = make_args(ctx, p);
+  if (code == ST_CFL || code == ST_NONFINITE) {
+    CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
+    CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    dispatch<LaunchReduce>(ctx->cfg.system, ctx, a);
+    CKL();
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, ctx->dscal, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double smax;
+    memcpy(&smax, &h[0], sizeof smax);
+    if (code == ST_CFL) {
+      ctx->err_value = smax;
+      CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
+      dispatch<LaunchArgmax>(ctx->cfg.system, ctx, a, smax, ctx->dscal + 3);
+      CKL();
+    }
+    CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return FV2D_OK;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+fv2d_status fv2d_version(int32_t* major, int32_t* minor) {
+  if (major) *major = FV2D_VERSION_MAJOR;
+  if (minor) *minor = FV2D_VERSION_MINOR;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_config_default(fv2d_config* cfg, int32_t nx, int32_t ny, int32_t system) {
+  if (!cfg) return FV2D_E_ARG;
+  memset(cfg, 0, sizeof *cfg);
+  cfg->nx = nx;
+  cfg->ny = ny;
+  cfg->system = system;
+  cfg->nvar = nvar_of(system);
+  cfg->x0 = 0.0; cfg->x1 = 1.0; cfg->y0 = 0.0; cfg->y1 = 1.0;
+  if (system == FV2D_EULER) cfg->param[0] = 1.4;
+  if (system == FV2D_ADVECTION) { cfg->param[0] = 1.0; cfg->param[1] = 0.5; }
+  if (system == FV2D_SPRAY) { cfg->param[0] = 1.0; cfg->param[1] = 1.0; }
+  cfg->rank = 0;
+  cfg->nranks = 1;
+  cfg->nslabs = 1;
+  return cfg->nvar > 0 ? FV2D_OK : FV2D_E_ARG;
+}
+
+fv2d_status fv2d_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return FV2D_E_ARG;
+  if (!load_nccl()) return FV2D_E_NCCL;
+  ncclUniqueId u;
+  if (g_nccl.GetUniqueId(&u) != ncclSuccess) return FV2D_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(id, &u, 128);
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
+  if (!ctx) return FV2D_OK;
+  cudaSetDevice(ctx->cfg.device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (int s = 0; s < kMaxSlabs; ++s)
+    for (int p = 0; p < 2; ++p) {
+      if (ctx->buf[s][p]) cudaFree(ctx->buf[s][p]);
+      if (ctx->gs[s][p]) cudaFree(ctx->gs[s][p]);
+      if (ctx->gn[s][p]) cudaFree(ctx->gn[s][p]);
+    }
+  if (ctx->send_s) cudaFree(ctx->send_s);
+  if (ctx->send_n) cudaFree(ctx->send_n);
+  if (ctx->staging) cudaFree(ctx->staging);
+  if (ctx->dscal) cudaFree(ctx->dscal);
+  if (ctx->done) cudaFree(ctx->done);
+  if (ctx->dt_dev) cudaFree(ctx->dt_dev);
+  if (ctx->dt_log) cudaFree(ctx->dt_log);
+  if (ctx->newton) cudaFree(ctx->newton);
+  if (ctx->trig) cudaFree(ctx->trig);
+  if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  delete ctx;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void* cuda_stream, fv2d_ctx** out) {
+  if (!cfg_in || !out) return FV2D_E_ARG;
+  *out = nullptr;
+  const fv2d_config& c = *cfg_in;
+  const int nv = nvar_of(c.system);
+  if (nv < 0 || c.nvar != nv || c.nx < 1 || c.ny < 1 || c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks ||
+      c.nslabs < 1 || c.nslabs > kMaxSlabs || (c.nranks > 1 && c.nslabs != 1) ||
+      c.ny % (c.nranks * c.nslabs) != 0 || !(c.x1 > c.x0) || !(c.y1 > c.y0) || c.bc_x < 0 || c.bc_x > 2 ||
+      c.bc_y < 0 || c.bc_y > 2)
+    return FV2D_E_ARG;
+  if (c.system == FV2D_ADVECTION && (c.bc_x == FV2D_BC_WALL || c.bc_y == FV2D_BC_WALL)) return FV2D_E_ARG;
+  if (c.system == FV2D_EULER && !(c.param[0] > 1.0)) return FV2D_E_ARG;
+  if (c.system == FV2D_SPRAY && !(c.param[1] > 0.0)) return FV2D_E_ARG;
+  for (int k = 0; k < 7; ++k)
+    if (c.reserved[k] != 0) return FV2D_E_ARG;
+  const long long H = c.ny / (c.nranks * c.nslabs);
+  if (H < 1) return FV2D_E_ARG;
+  if (c.nranks > 1 && (!nccl_id || !load_nccl())) return FV2D_E_NCCL;
+
+  fv2d_ctx* ctx = new fv2d_ctx();
+  ctx->cfg = c;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  ctx->nv = nv;
+  ctx->nx = c.nx;
+  ctx->H = (int)H;
+  ctx->pitch = (c.nx + 31) / 32 * 32;
+  ctx->plane = (long long)ctx->pitch * H;
+  ctx->nslabs = c.nslabs;
+  ctx->G = c.nranks * c.nslabs;
+  ctx->dx = (c.x1 - c.x0) / c.nx;
+  ctx->dy = (c.y1 - c.y0) / c.ny;
+  ctx->hmin = ctx->dx < ctx->dy ? ctx->dx : ctx->dy;
+
+  auto fail = [&](fv2d_status s) {
+    std::string m = ctx->err;
+    fv2d_destroy(ctx);
+    (void)m;
+    return s;
+  };
+#define CKC(call)                                                                                  \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      fprintf(stderr, "fv2d_create: %s failed: %s\n", #call, cudaGetErrorString(e_));              \
+      return fail(FV2D_E_CUDA);                                                                    \
+    }                                                                                              \
+  } while (0)
+  CKC(cudaSetDevice(c.device));
+  const size_t state_bytes = (size_t)nv * ctx->plane * sizeof(double);
+  const size_t row_bytes = (size_t)nv * ctx->pitch * sizeof(double);
+  for (int s = 0; s < ctx->nslabs; ++s)
+    for (int p = 0; p < 2; ++p) {
+      CKC(cudaMalloc(&ctx->buf[s][p], state_bytes));
+      CKC(cudaMemset(ctx->buf[s][p], 0, state_bytes));
+      CKC(cudaMalloc(&ctx->gs[s][p], row_bytes));
+      CKC(cudaMalloc(&ctx->gn[s][p], row_bytes));
+      CKC(cudaMemset(ctx->gs[s][p], 0, row_bytes));
+      CKC(cudaMemset(ctx->gn[s][p], 0, row_bytes));
+    }
+  if (c.nranks > 1) {
+    CKC(cudaMalloc(&ctx->send_s, row_bytes));
+    CKC(cudaMalloc(&ctx->send_n, row_bytes));
+    CKC(cudaMemset(ctx->send_s, 0, row_bytes));
+    CKC(cudaMemset(ctx->send_n, 0, row_bytes));
+  }
+  CKC(cudaMalloc(&ctx->dscal, 8 * sizeof(unsigned long long)));
+  CKC(cudaMemset(ctx->dscal, 0, 8 * sizeof(unsigned long long)));
+  CKC(cudaMemset(ctx->dscal + 3, 0xff, sizeof(unsigned long long)));
+  CKC(cudaMalloc(&ctx->done, sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->done, 0, sizeof(unsigned int)));
+  CKC(cudaMalloc(&ctx->dt_dev, sizeof(double)));
+  CKC(cudaMemset(ctx->dt_dev, 0, sizeof(double)));
+  CKC(cudaMalloc(&ctx->newton, sizeof(unsigned long long)));
+  CKC(cudaMemset(ctx->newton, 0, sizeof(unsigned long long)));
+  if (c.system == FV2D_SPRAY) {
+    CKC(cudaMalloc(&ctx->trig, (size_t)(2 * c.nx + 2 * c.ny) * sizeof(double)));
+    trig_table_kernel<<<(c.nx + 255) / 256, 256>>>(ctx->trig, ctx->trig + c.nx, c.nx, c.x0, ctx->dx);
+    trig_table_kernel<<<(c.ny + 255) / 256, 256>>>(ctx->trig + 2 * c.nx, ctx->trig + 2 * c.nx + c.ny, c.ny, c.y0,
+                                                    ctx->dy);
+    CKC(cudaGetLastError());
+    static bool gl_done = false;
+    if (!gl_done) {
+      double t[24], wt[24][8];
+      gl24_table(t, wt);
+      CKC(cudaMemcpyToSymbol(c_gl_t, t, sizeof t));
+      CKC(cudaMemcpyToSymbol(c_gl_wt, wt, sizeof wt));
+      gl_done = true;
+    }
+  }
+  // Dirichlet ghost rows are constant for the whole run.
+  if (c.bc_y == FV2D_BC_DIRICHLET) {
+    for (int s = 0; s < ctx->nslabs; ++s) {
+      const int g = c.rank * c.nslabs + s;
+      for (int p = 0; p < 2; ++p) {
+        if (g == 0)
+          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ctx->gs[s][p], nv, c.nx, ctx->pitch, c.dirichlet[0],
+                                                             c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
+                                                             c.dirichlet[4], c.dirichlet[5]);
+        if (g == ctx->G - 1)
+          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ctx->gn[s][p], nv, c.nx, ctx->pitch, c.dirichlet[0],
+                                                             c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
+                                                             c.dirichlet[4], c.dirichlet[5]);
+      }
+    }
+    CKC(cudaGetLastError());
+  }
+  CKC(cudaDeviceSynchronize());
+  if (c.nranks > 1) {
+    ncclUniqueId u;
+    memcpy(&u, nccl_id, sizeof u);
+    if (g_nccl.CommInitRank(&ctx->comm, c.nranks, u, c.rank) != ncclSuccess) return fail(FV2D_E_NCCL);
+  }
+#undef CKC
+  *out = ctx;
+  return FV2D_OK;
+}
+
+static fv2d_status after_set_state(fv2d_ctx* ctx) {
+  // ghost rows of parity 0 from the new W^0, then reset the counters
+  ctx->steps = 0;
+  StepArgs a = make_args(ctx, 1);  // "reading" parity 1 means ghost targets of parity 0
+  for (int s = 0; s < ctx->nslabs; ++s) a.slab[s].in = ctx->buf[s][0];
+  fill_halo_kernel<<<dim3((ctx->nx + 127) / 128, 1, ctx->nslabs), 128, 0, ctx->stream>>>(a, ctx->nv);
+  CKL();
+  fv2d_status st = exchange(ctx, 0);
+  if (st) return st;
+  unsigned long long init[8] = {0, 0, 0, ~0ull, 0, 0, 0, 0};
+  CK(cudaMemcpyAsync(ctx->dscal, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->done, 0, sizeof(unsigned int), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dt_dev, 0, sizeof(double), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->has_state = true;
+  ctx->dt_valid = false;
+  ctx->err.clear();
+  ctx->err_step = ctx->err_cell = -1;
+  return FV2D_OK;
+}
+
+static fv2d_status ensure_staging(fv2d_ctx* ctx) {
+  const size_t need = (size_t)ctx->nv * ctx->nx * ctx->H * ctx->nslabs * sizeof(double);
+  if (ctx->staging_bytes >= need) return FV2D_OK;
+  if (ctx->staging) CK(cudaFree(ctx->staging));
+  ctx->staging = nullptr;
+  CK(cudaMalloc(&ctx->staging, need));
+  ctx->staging_bytes = need;
+  return FV2D_OK;
+}
+
+static fv2d_status upload(fv2d_ctx* ctx, const double* src, fv2d_layout layout, cudaMemcpyKind kind) {
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int nv = ctx->nv, nx = ctx->nx, H = ctx->H;
+  if (layout == FV2D_SOA) {
+    // SoA [nv][ny_local][nx]: per variable, slab rows are contiguous in the source
+    const long long nyl = (long long)H * ctx->nslabs;
+    for (int s = 0; s < ctx->nslabs; ++s)
+      for (int v = 0; v < nv; ++v)
+        CK(cudaMemcpy2DAsync(ctx->buf[s][0] + v * ctx->plane, ctx->pitch * sizeof(double),
+                             src + (size_t)v * nyl * nx + (size_t)s * H * nx, nx * sizeof(double),
+                             nx * sizeof(double), H, kind, ctx->stream));
+  } else {
+    fv2d_status st = ensure_staging(ctx);
+    if (st) return st;
+    const size_t bytes = (size_t)nv * nx * H * ctx->nslabs * sizeof(double);
+    CK(cudaMemcpyAsync(ctx->staging, src, bytes, kind, ctx->stream));
+    for (int s = 0; s < ctx->nslabs; ++s) {
+      aos_to_soa_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->staging + (size_t)s * H * nx * nv, ctx->buf[s][0], nv,
+                                                          nx, H, ctx->pitch, ctx->plane);
+      CKL();
+    }
+  }
+  return after_set_state(ctx);
+}
+
+fv2d_status fv2d_set_state(fv2d_ctx* ctx, const double* host, fv2d_layout layout) {
+  if (!ctx || !host || (layout != FV2D_AOS && layout != FV2D_SOA)) return FV2D_E_ARG;
+  return upload(ctx, host, layout, cudaMemcpyHostToDevice);
+}
+
+fv2d_status fv2d_set_state_device(fv2d_ctx* ctx, const double* dev, fv2d_layout layout) {
+  if (!ctx || !dev || (layout != FV2D_AOS && layout != FV2D_SOA)) return FV2D_E_ARG;
+  return upload(ctx, dev, layout, cudaMemcpyDeviceToDevice);
+}
+
+fv2d_status fv2d_get_state(fv2d_ctx* ctx, double* host, fv2d_layout layout) {
+  if (!ctx || !host || (layout != FV2D_AOS && layout != FV2D_SOA)) return FV2D_E_ARG;
+  if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
+  CK(cudaSetDevice(ctx->cfg.device));
+  unsigned long long st;
+  fv2d_status s0 = read_status(ctx, &st);
+  if (s0) return s0;
+  const int p = st ? (int)((st & 0x00FFFFFFFFFFFFFFull) & 1) : cur_parity(ctx);
+  const int nv = ctx->nv, nx = ctx->nx, H = ctx->H;
+  if (layout == FV2D_SOA) {
+    const long long nyl = (long long)H * ctx->nslabs;
+    for (int s = 0; s < ctx->nslabs; ++s)
+      for (int v = 0; v < nv; ++v)
+        CK(cudaMemcpy2DAsync(host + (size_t)v * nyl * nx + (size_t)s * H * nx, nx * sizeof(double),
+                             ctx->buf[s][p] + v * ctx->plane, ctx->pitch * sizeof(double), nx * sizeof(double), H,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    fv2d_status s1 = ensure_staging(ctx);
+    if (s1) return s1;
+    for (int s = 0; s < ctx->nslabs; ++s) {
+      soa_to_aos_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->buf[s][p], ctx->staging + (size_t)s * H * nx * nv, nv,
+                                                          nx, H, ctx->pitch, ctx->plane);
+      CKL();
+    }
+    CK(cudaMemcpyAsync(host, ctx->staging, (size_t)nv * nx * H * ctx->nslabs * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return report(ctx, st);
+}
+
+fv2d_status fv2d_compute_dt(fv2d_ctx* ctx, double cfl, double* dt, double* smax) {
+  if (!ctx || !(cfl > 0.0) || !(cfl <= 1.0)) return FV2D_E_ARG;
+  if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
+  CK(cudaSetDevice(ctx->cfg.device));
+  unsigned long long st;
+  fv2d_status s0 = read_status(ctx, &st);
+  if (s0) return s0;
+  if (st) return report(ctx, st);
+  double s;
+  unsigned long long pend;
+  s0 = reduce_current(ctx, &s, &pend);
+  if (s0) return s0;
+  if (smax) *smax = s;
+  if (pend) {
+    const unsigned long long w = ((unsigned long long)ST_NONFINITE << 56) | (unsigned long long)ctx->steps;
+    return report(ctx, w);
+  }
+  const double d = (cfl * ctx->hmin) / s;
+  if (dt) *dt = d;
+  CK(cudaMemcpyAsync(ctx->dt_dev, &d, sizeof d, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->dt_valid = true;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_check_dt(fv2d_ctx* ctx, double dt, double* smax) {
+  if (!ctx || !(dt > 0.0)) return FV2D_E_ARG;
+  if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
+  CK(cudaSetDevice(ctx->cfg.device));
+  double s;
+  unsigned long long pend;
+  fv2d_status s0 = reduce_current(ctx, &s, &pend);
+  if (s0) return s0;
+  if (smax) *smax = s;
+  if (pend) return set_err(ctx, FV2D_E_NONFINITE, "non-admissible state");
+  if (dt * s > ctx->hmin) {
+    ctx->err_value = s;
+    return set_err(ctx, FV2D_E_CFL, "dt*smax = %.17g > min(dx,dy) = %.17g", dt * s, ctx->hmin);
+  }
+  return FV2D_OK;
+}
+
+static fv2d_status prof_flush(fv2d_ctx* ctx) {
+  if (ctx->ev_used == 0) return FV2D_OK;
+  CK(cudaEventSynchronize(ctx->ev_pool[ctx->ev_used - 1]));
+  for (size_t k = 0; k + 1 < ctx->ev_used; k += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev_pool[k], ctx->ev_pool[k + 1]));
+    ctx->prof_ms += ms;
+    ctx->prof_n += 1;
+  }
+  ctx->ev_used = 0;
+  return FV2D_OK;
+}
+
+static fv2d_status prof_events(fv2d_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1) {
+  if (ctx->ev_used + 2 > 4096) {
+    fv2d_status st = prof_flush(ctx);
+    if (st) return st;
+  }
+  while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->ev_pool.push_back(e);
+  }
+  *e0 = ctx->ev_pool[ctx->ev_used];
+  *e1 = ctx->ev_pool[ctx->ev_used + 1];
+  ctx->ev_used += 2;
+  return FV2D_OK;
+}
+
+static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double cfl, int32_t nsteps) {
+  fv2d_status st = ensure_dt_log(ctx, ctx->steps + nsteps);
+  if (st) return st;
+  const bool split = ctx->cfg.system == FV2D_SPRAY && (ctx->cfg.flags & FV2D_FLAG_SPLIT_SOURCE);
+  for (int32_t k = 0; k < nsteps; ++k) {
+    const int p = cur_parity(ctx);
+    StepArgs a = make_args(ctx, p);
+    a.adaptive = adaptive;
+    a.dt = dt;
+    a.cfl = cfl;
+    a.step = ctx->steps;
+    if (split || ctx->cfg.nranks > 1) a.fused_finalize = 0;
+    if (split) a.fuse_source = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->profiling) {
+      st = prof_events(ctx, &e0, &e1);
+      if (st) return st;
+      CK(cudaEventRecord(e0, ctx->stream));
+    }
+    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, a);
+    CKL();
+    if (ctx->profiling) CK(cudaEventRecord(e1, ctx->stream));
+    if (split) {
+      StepArgs b = a;
+      for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = ctx->buf[s][1 - p];
+      dim3 grid((ctx->nx + 127) / 128, ctx->H, ctx->nslabs);
+      spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt);
+      CKL();
+    }
+    if (ctx->cfg.nranks > 1) {
+      st = exchange(ctx, 1 - p);
+      if (st) return st;
+      st = allreduce_scalars(ctx);
+      if (st) return st;
+      finalize_kernel<<<1, 32, 0, ctx->stream>>>(a, ctx->dscal + 4);
+      CKL();
+    } else if (!a.fused_finalize) {
+      finalize_kernel<<<1, 32, 0, ctx->stream>>>(a, nullptr);
+      CKL();
+    }
+    ctx->steps += 1;
+  }
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_step(fv2d_ctx* ctx, double dt, int32_t nsteps) {
+  if (!ctx || !(dt > 0.0) || nsteps < 0 || !std::isfinite(dt)) return FV2D_E_ARG;
+  if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
+  CK(cudaSetDevice(ctx->cfg.device));
+  return launch_steps(ctx, 0, dt, 0.0, nsteps);
+}
+
+fv2d_status fv2d_step_adaptive(fv2d_ctx* ctx, double cfl, int32_t nsteps, double* dt_log) {
+  if (!ctx || !(cfl > 0.0) || !(cfl <= 1.0) || nsteps < 0) return FV2D_E_ARG;
+  if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
+  if (ctx->cfg.system == FV2D_SPRAY && (ctx->cfg.flags & FV2D_FLAG_SPLIT_SOURCE))
+    return set_err(ctx, FV2D_E_ARG, "adaptive dt needs the fused spray source (smax of the post-source state)");
+  CK(cudaSetDevice(ctx->cfg.device));
+  if (!ctx->dt_valid) {
+    double d, s;
+    fv2d_status st = fv2d_compute_dt(ctx, cfl, &d, &s);
+    if (st) return st;
+  }
+  const long long first = ctx->steps;
+  fv2d_status st = launch_steps(ctx, 1, 0.0, cfl, nsteps);
+  if (st) return st;
+  if (dt_log && nsteps > 0) {
+    CK(cudaMemcpyAsync(dt_log, ctx->dt_log + first, nsteps * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long s;
+    st = read_status(ctx, &s);
+    if (st) return st;
+    if (s) return report(ctx, s);
+  }
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
+  if (!ctx || !(dt > 0.0)) return FV2D_E_ARG;
+  if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
+  if (ctx->cfg.system != FV2D_SPRAY) return FV2D_OK;  // S = 0
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int p = cur_parity(ctx);
+  // in place on parity p: halo targets are the ghost buffers of parity p
+  StepArgs b = make_args(ctx, 1 - p);
+  for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = ctx->buf[s][p];
+  b.step = ctx->steps;
+  dim3 grid((ctx->nx + 127) / 128, ctx->H, ctx->nslabs);
+  spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt);
+  CKL();
+  fv2d_status st = exchange(ctx, p);
+  if (st) return st;
+  promote_pending_kernel<<<1, 32, 0, ctx->stream>>>(ctx->dscal + 1, ctx->dscal + 2);
+  CKL();
+  ctx->dt_valid = false;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_synchronize(fv2d_ctx* ctx) {
+  if (!ctx) return FV2D_E_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  unsigned long long st;
+  fv2d_status s0 = read_status(ctx, &st);
+  if (s0) return s0;
+  return report(ctx, st);
+}
+
+fv2d_status fv2d_device_state(fv2d_ctx* ctx, int32_t slab, double** d_ptr, int64_t* pitch, int64_t* plane_stride,
+                              int32_t* ny_slab) {
+  if (!ctx || slab < 0 || slab >= ctx->nslabs) return FV2D_E_ARG;
+  if (d_ptr) *d_ptr = ctx->buf[slab][cur_parity(ctx)];
+  if (pitch) *pitch = ctx->pitch;
+  if (plane_stride) *plane_stride = ctx->plane;
+  if (ny_slab) *ny_slab = ctx->H;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_last_error(fv2d_ctx* ctx, char* buf, size_t n, int64_t* step, int64_t* cell, double* value) {
+  if (!ctx) return FV2D_E_ARG;
+  unsigned long long st = 0;
+  if (ctx->has_state && read_status(ctx, &st) == FV2D_OK && st) {
+    report(ctx, st);
+    diagnose(ctx, st);
+    unsigned long long bc = ~0ull;
+    cudaMemcpy(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost);
+    ctx->err_cell = bc == ~0ull ? -1 : (long long)bc;
+  }
+  if (buf && n) {
+    snprintf(buf, n, "%s", ctx->err.c_str());
+  }
+  if (step) *step = ctx->err_step;
+  if (cell) *cell = ctx->err_cell;
+  if (value) *value = ctx->err_value;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_set_profiling(fv2d_ctx* ctx, int32_t enable) {
+  if (!ctx) return FV2D_E_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  fv2d_status st = prof_flush(ctx);
+  if (st) return st;
+  ctx->profiling = enable != 0;
+  ctx->prof_ms = 0.0;
+  ctx->prof_n = 0;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out) {
+  if (!ctx || !out) return FV2D_E_ARG;
+  fv2d_status st = prof_flush(ctx);
+  if (st) return st;
+  out->step_kernel_ms = ctx->prof_ms;
+  out->step_kernels_timed = ctx->prof_n;
+  out->steps = ctx->steps;
+  out->kernel_launches = ctx->launches;
+  unsigned long long ni = 0;
+  if (ctx->newton) cudaMemcpy(&ni, ctx->newton, sizeof ni, cudaMemcpyDeviceToHost);
+  out->newton_iters = (int64_t)ni;
+  double d = 0;
+  if (ctx->dt_dev) cudaMemcpy(&d, ctx->dt_dev, sizeof d, cudaMemcpyDeviceToHost);
+  out->dt = d;
+  return FV2D_OK;
+}
+
+}  // extern "C"

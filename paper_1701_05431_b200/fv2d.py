@@ -1,0 +1,233 @@
+"""Thin ctypes binding of libfv2d.so (include/fv2d.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; there is no
+Python or CPU fallback -- if the library cannot be built/loaded, import of the
+binding raises.  Names follow the C ABI (fv2d_create -> Solver(...),
+fv2d_step -> Solver.step, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+OK, E_ARG, E_CFL, E_NONFINITE, E_RECON, E_CUDA, E_NCCL, E_STATE = range(8)
+ADVECTION, EULER, SPRAY = 0, 1, 2
+BC_PERIODIC, BC_DIRICHLET, BC_WALL = 0, 1, 2
+AOS, SOA = 0, 1
+FLAG_NAIVE, FLAG_SPLIT_SOURCE = 0x1, 0x2
+NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
+_NAMES = {OK: "OK", E_ARG: "E_ARG", E_CFL: "E_CFL", E_NONFINITE: "E_NONFINITE", E_RECON: "E_RECON",
+          E_CUDA: "E_CUDA", E_NCCL: "E_NCCL", E_STATE: "E_STATE"}
+
+
+class Config(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nvar", C.c_int32), ("system", C.c_int32),
+                ("bc_x", C.c_int32), ("bc_y", C.c_int32),
+                ("x0", C.c_double), ("x1", C.c_double), ("y0", C.c_double), ("y1", C.c_double),
+                ("param", C.c_double * 8), ("dirichlet", C.c_double * 6),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("nslabs", C.c_int32), ("device", C.c_int32),
+                ("flags", C.c_uint32), ("reserved", C.c_int32 * 7)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("kernel_launches", C.c_int64), ("newton_iters", C.c_int64),
+                ("dt", C.c_double), ("step_kernel_ms", C.c_double), ("step_kernels_timed", C.c_int64)]
+
+
+_LIB = None
+
+
+def lib():
+    """Load libfv2d.so (building it in-tree first if missing or stale)."""
+    global _LIB
+    if _LIB is None:
+        path = _build.build()
+        L = C.CDLL(path)
+        P = C.POINTER
+        vp = C.c_void_p
+        d = P(C.c_double)
+        L.fv2d_version.argtypes = [P(C.c_int32), P(C.c_int32)]
+        L.fv2d_config_default.argtypes = [P(Config), C.c_int32, C.c_int32, C.c_int32]
+        L.fv2d_nccl_unique_id.argtypes = [C.c_char_p]
+        L.fv2d_create.argtypes = [P(Config), C.c_char_p, vp, P(vp)]
+        L.fv2d_destroy.argtypes = [vp]
+        L.fv2d_set_state.argtypes = [vp, vp, C.c_int]
+        L.fv2d_set_state_device.argtypes = [vp, vp, C.c_int]
+        L.fv2d_get_state.argtypes = [vp, vp, C.c_int]
+        L.fv2d_compute_dt.argtypes = [vp, C.c_double, d, d]
+        L.fv2d_check_dt.argtypes = [vp, C.c_double, d]
+        L.fv2d_step.argtypes = [vp, C.c_double, C.c_int32]
+        L.fv2d_step_adaptive.argtypes = [vp, C.c_double, C.c_int32, d]
+        L.fv2d_apply_source.argtypes = [vp, C.c_double]
+        L.fv2d_synchronize.argtypes = [vp]
+        L.fv2d_device_state.argtypes = [vp, C.c_int32, P(vp), P(C.c_int64), P(C.c_int64), P(C.c_int32)]
+        L.fv2d_last_error.argtypes = [vp, C.c_char_p, C.c_size_t, P(C.c_int64), P(C.c_int64), d]
+        L.fv2d_get_stats.argtypes = [vp, P(Stats)]
+        L.fv2d_set_profiling.argtypes = [vp, C.c_int32]
+        for name in ("fv2d_version", "fv2d_config_default", "fv2d_nccl_unique_id", "fv2d_create", "fv2d_destroy",
+                     "fv2d_set_state", "fv2d_set_state_device", "fv2d_get_state", "fv2d_compute_dt",
+                     "fv2d_check_dt", "fv2d_step", "fv2d_step_adaptive", "fv2d_apply_source",
+                     "fv2d_synchronize", "fv2d_device_state", "fv2d_last_error", "fv2d_get_stats",
+                     "fv2d_set_profiling"):
+            getattr(L, name).restype = C.c_int
+        _LIB = L
+    return _LIB
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+class FV2DError(RuntimeError):
+    def __init__(self, code, message="", step=-1, cell=-1, value=float("nan")):
+        super().__init__(f"fv2d {_NAMES.get(code, code)}: {message} (step {step}, cell {cell})")
+        self.code, self.message, self.step, self.cell, self.value = code, message, step, cell, value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib().fv2d_nccl_unique_id(buf)
+    if rc != OK:
+        raise FV2DError(rc, "ncclGetUniqueId")
+    return buf.raw
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Solver:
+    """One context of libfv2d (fv2d_create ... fv2d_destroy)."""
+
+    def __init__(self, nx, ny, system=EULER, *, x0=0.0, x1=1.0, y0=0.0, y1=1.0, param=None,
+                 bc_x=BC_PERIODIC, bc_y=BC_PERIODIC, dirichlet=(), rank=0, nranks=1, nslabs=1, device=0,
+                 flags=0, nccl_id: bytes | None = None, stream: int | None = None):
+        L = lib()
+        cfg = Config()
+        rc = L.fv2d_config_default(C.byref(cfg), nx, ny, system)
+        if rc != OK:
+            raise FV2DError(rc, "config_default")
+        cfg.x0, cfg.x1, cfg.y0, cfg.y1 = x0, x1, y0, y1
+        if param is not None:
+            for k in range(8):
+                cfg.param[k] = 0.0
+            for k, v in enumerate(param):
+                cfg.param[k] = v
+        for k, v in enumerate(dirichlet):
+            cfg.dirichlet[k] = v
+        cfg.bc_x, cfg.bc_y = bc_x, bc_y
+        cfg.rank, cfg.nranks, cfg.nslabs, cfg.device, cfg.flags = rank, nranks, nslabs, device, flags
+        self.cfg = cfg
+        self.nx, self.ny, self.nv, self.system = nx, ny, NVAR[system], system
+        self.ny_local = ny // nranks
+        h = C.c_void_p()
+        rc = L.fv2d_create(C.byref(cfg), nccl_id, C.c_void_p(stream or 0), C.byref(h))
+        if rc != OK:
+            raise FV2DError(rc, "fv2d_create")
+        self._h = h
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fv2d_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- errors
+    def last_error(self):
+        buf = C.create_string_buffer(512)
+        st, cell = C.c_int64(-1), C.c_int64(-1)
+        val = C.c_double(float("nan"))
+        lib().fv2d_last_error(self._h, buf, 512, C.byref(st), C.byref(cell), C.byref(val))
+        return {"message": buf.value.decode(), "step": st.value, "cell": cell.value, "value": val.value}
+
+    def _check(self, rc, what=""):
+        if rc != OK:
+            e = self.last_error() if self._h else {"message": what, "step": -1, "cell": -1, "value": float("nan")}
+            raise FV2DError(rc, e["message"] or what, e["step"], e["cell"], e["value"])
+
+    # -- state
+    def _shape(self, layout):
+        return (self.ny_local, self.nx, self.nv) if layout == AOS else (self.nv, self.ny_local, self.nx)
+
+    def set_state(self, W: np.ndarray, layout: int = AOS):
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        if W.shape != self._shape(layout):
+            raise ValueError(f"state shape {W.shape} != {self._shape(layout)}")
+        self._check(lib().fv2d_set_state(self._h, W.ctypes.data, layout), "set_state")
+
+    def set_state_ptr(self, ptr: int, layout: int = AOS, device: bool = False):
+        fn = lib().fv2d_set_state_device if device else lib().fv2d_set_state
+        self._check(fn(self._h, C.c_void_p(ptr), layout), "set_state")
+
+    def get_state(self, layout: int = AOS, out: np.ndarray | None = None, raise_on_error: bool = True):
+        if out is None:
+            out = np.empty(self._shape(layout))
+        rc = lib().fv2d_get_state(self._h, out.ctypes.data, layout)
+        if raise_on_error:
+            self._check(rc, "get_state")
+        return out
+
+    def get_state_ptr(self, ptr: int, layout: int = AOS):
+        self._check(lib().fv2d_get_state(self._h, C.c_void_p(ptr), layout), "get_state")
+
+    def device_state(self, slab: int = 0):
+        p, pitch, plane, ny = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int32()
+        self._check(lib().fv2d_device_state(self._h, slab, C.byref(p), C.byref(pitch), C.byref(plane),
+                                            C.byref(ny)))
+        return p.value, pitch.value, plane.value, ny.value
+
+    # -- the hot path
+    def compute_dt(self, cfl: float):
+        dt, s = C.c_double(), C.c_double()
+        self._check(lib().fv2d_compute_dt(self._h, cfl, C.byref(dt), C.byref(s)), "compute_dt")
+        return dt.value, s.value
+
+    def check_dt(self, dt: float) -> float:
+        s = C.c_double()
+        self._check(lib().fv2d_check_dt(self._h, dt, C.byref(s)), "check_dt")
+        return s.value
+
+    def step(self, dt: float, nsteps: int = 1):
+        self._check(lib().fv2d_step(self._h, dt, nsteps), "step")
+
+    def step_adaptive(self, cfl: float, nsteps: int = 1, log: bool = True):
+        if log:
+            buf = np.zeros(max(1, nsteps))
+            self._check(lib().fv2d_step_adaptive(self._h, cfl, nsteps, _dp(buf)), "step_adaptive")
+            return buf[:nsteps]
+        self._check(lib().fv2d_step_adaptive(self._h, cfl, nsteps, None), "step_adaptive")
+        return None
+
+    def apply_source(self, dt: float):
+        self._check(lib().fv2d_apply_source(self._h, dt), "apply_source")
+
+    def synchronize(self):
+        self._check(lib().fv2d_synchronize(self._h), "synchronize")
+
+    def status(self) -> int:
+        return lib().fv2d_synchronize(self._h)
+
+    def set_profiling(self, enable: bool = True):
+        self._check(lib().fv2d_set_profiling(self._h, 1 if enable else 0), "set_profiling")
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(lib().fv2d_get_stats(self._h, C.byref(s)), "get_stats")
+        return {"steps": s.steps, "kernel_launches": s.kernel_launches, "newton_iters": s.newton_iters,
+                "dt": s.dt, "step_kernel_ms": s.step_kernel_ms, "step_kernels_timed": s.step_kernels_timed}

@@ -1,0 +1,63 @@
+"""CPU checks of the boundary: the C-ABI library builds for sm_100a, loads, and
+exports every symbol include/fv2d.h declares; host-side argument validation.
+(No compute calls: there is no GPU here.)"""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1701_05431_b200 import fv2d
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "fv2d.h")).read()
+    return sorted(set(re.findall(r"^fv2d_status\s+(fv2d_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = fv2d.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", fv2d.lib_path()], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (fv2d_\w+)", out))
+    for s in syms:
+        assert s in exported, s
+        assert getattr(L, s) is not None
+
+
+def test_sass_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", fv2d.lib_path()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_config_struct_matches_header():
+    # 6 int32 + 4 doubles + 8 + 6 doubles + 4 int32 + uint32 + 7 int32 (with padding)
+    assert C.sizeof(fv2d.Config) == 24 + 32 + 64 + 48 + 16 + 4 + 28
+    cfg = fv2d.Config()
+    assert fv2d.lib().fv2d_config_default(C.byref(cfg), 64, 32, fv2d.EULER) == fv2d.OK
+    assert (cfg.nx, cfg.ny, cfg.nvar, cfg.param[0], cfg.nranks, cfg.nslabs) == (64, 32, 4, 1.4, 1, 1)
+    assert fv2d.lib().fv2d_config_default(C.byref(cfg), 64, 32, 7) == fv2d.E_ARG
+
+
+def test_create_validates_before_touching_the_device():
+    L = fv2d.lib()
+    h = C.c_void_p()
+    cfg = fv2d.Config()
+    L.fv2d_config_default(C.byref(cfg), 64, 30, fv2d.EULER)
+    cfg.nslabs = 4                      # 30 % 4 != 0
+    assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
+    cfg.nslabs = 1
+    cfg.nvar = 3                        # nvar mismatch
+    assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
+    cfg.nvar = 4
+    cfg.param[0] = 1.0                  # gamma <= 1
+    assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
+    L.fv2d_config_default(C.byref(cfg), 8, 8, fv2d.ADVECTION)
+    cfg.bc_x = fv2d.BC_WALL             # wall undefined for advection
+    assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
+    assert L.fv2d_step(None, 1e-3, 1) == fv2d.E_ARG
+    assert L.fv2d_destroy(None) == fv2d.OK

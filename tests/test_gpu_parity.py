@@ -1,0 +1,268 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same
+seeded inputs.  Gate (BASELINE north_star, R27): relative max-norm error
+<= 1e-12 per step and <= 1e-10 after 100 steps, dt sequences identical (==).
+The exact build (no FMA, CEO) is expected to be bitwise; the tests assert the
+formal tolerance and report the bitwise status separately where it is a claim."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1701_05431_b200 import fv2d, inputs
+
+pytestmark = pytest.mark.gpu
+G = 1.4
+
+
+def relerr(a, b):
+    """max_v ||a_v - b_v||_inf / ||b_v||_inf; a variable with zero norm must match exactly."""
+    e = 0.0
+    for v in range(b.shape[-1]):
+        nb = np.abs(b[..., v]).max()
+        d = np.abs(a[..., v] - b[..., v]).max()
+        if nb == 0:
+            assert d == 0
+        else:
+            e = max(e, d / nb)
+    return e
+
+
+def solver_for(cfg: O.Config, **kw):
+    return fv2d.Solver(cfg.nx, cfg.ny, cfg.system, x0=cfg.x0, x1=cfg.x1, y0=cfg.y0, y1=cfg.y1,
+                       param=cfg.param, bc_x=cfg.bc_x, bc_y=cfg.bc_y, dirichlet=cfg.dirichlet, **kw)
+
+
+def gpu_run(cfg, W0, nsteps, mode, value, **kw):
+    with solver_for(cfg, **kw) as s:
+        s.set_state(W0)
+        if mode == O.ADAPTIVE:
+            log = s.step_adaptive(value, nsteps)
+        else:
+            s.step(value, nsteps)
+            log = None
+        W = s.get_state()
+    return W, log
+
+
+CASES = {
+    "adv_dyadic_64": (O.Config(nx=64, ny=64, system=O.ADVECTION, param=(1.0, 0.5)),
+                      lambda: inputs.advection_dyadic(64, 64, seed=0), 0.5),
+    "adv_smooth_64": (O.Config(nx=64, ny=64, system=O.ADVECTION, param=(1.0, 0.5)),
+                      lambda: inputs.advection_smooth(64, 64), 0.5),
+    "euler_random_300x200": (O.Config(nx=300, ny=200, system=O.EULER, param=(G,), x1=1.5),
+                             lambda: inputs.euler_random(300, 200, seed=1), 0.45),
+    "euler_laxliu3_256": (O.Config(nx=256, ny=256, system=O.EULER, param=(G,)),
+                          lambda: inputs.euler_lax_liu3(256, 256), 0.45),
+    "euler_sod_wall_x_250x40": (O.Config(nx=250, ny=40, system=O.EULER, param=(G,), bc_x=O.BC_WALL),
+                                lambda: inputs.euler_sod_x(250, 40), 0.45),
+    "euler_sod_wall_y_40x250": (O.Config(nx=40, ny=250, system=O.EULER, param=(G,), bc_y=O.BC_WALL),
+                                lambda: inputs.euler_sod_x(250, 40).transpose(1, 0, 2)[..., [0, 2, 1, 3]].copy(),
+                                0.45),
+    "euler_dirichlet_130x70": (O.Config(nx=130, ny=70, system=O.EULER, param=(G,), bc_x=O.BC_DIRICHLET,
+                                        bc_y=O.BC_DIRICHLET, dirichlet=(1.0, 0.1, -0.2, 2.6)),
+                               lambda: inputs.euler_random(130, 70, seed=5), 0.45),
+    "euler_bell_128": (O.Config(nx=128, ny=128, system=O.EULER, param=(G,)),
+                       lambda: inputs.euler_bell(128, 128), 0.45),
+    "euler_3x3": (O.Config(nx=3, ny=3, system=O.EULER, param=(G,), x1=3.0, y1=3.0),
+                  lambda: np.array([[[1 + (3 * j + i) / 8, (i - 1) / 4, (j - 1) / 8, 2 + (i + 2 * j) / 16]
+                                     for i in range(3)] for j in range(3)]), 0.45),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_trajectory_100_steps_adaptive(name):
+    """100 independent steps on both sides: W^100 within 1e-10, dt log identical."""
+    cfg, ic, C = CASES[name]
+    W0 = ic()
+    ref = O.run(cfg, W0, 100, O.ADAPTIVE, C, dump_steps=(1, 10, 50, 100))
+    W, log = gpu_run(cfg, W0, 100, O.ADAPTIVE, C)
+    assert np.array_equal(log, ref.dt_log), "dt sequence differs"
+    e = relerr(W, ref.W)
+    assert e <= 1e-10
+    assert np.array_equal(W, ref.W), f"not bitwise (rel err {e:.3e})"
+
+
+@pytest.mark.parametrize("name", ["euler_random_300x200", "euler_laxliu3_256", "euler_sod_wall_x_250x40",
+                                  "adv_smooth_64"])
+def test_per_step_from_oracle_states(name):
+    """Feed the SAME W^k (from the oracle) to both sides, one step, <= 1e-12."""
+    cfg, ic, C = CASES[name]
+    ks = (0, 10, 50, 99)
+    ref = O.run(cfg, ic(), 100, O.ADAPTIVE, C, dump_steps=ks + tuple(k + 1 for k in ks))
+    for k in ks:
+        Wk = ref.dumps[k]
+        W1, log = gpu_run(cfg, Wk, 1, O.ADAPTIVE, C)
+        assert log[0] == ref.dt_log[k]
+        assert relerr(W1, ref.dumps[k + 1]) <= 1e-12
+        assert np.array_equal(W1, ref.dumps[k + 1])
+
+
+def test_fixed_dt_mode_matches_oracle():
+    cfg, ic, _ = CASES["euler_laxliu3_256"]
+    W0 = ic()
+    s, _ = O.smax(cfg, W0)
+    dt = 0.3 / 256 / s
+    ref = O.run(cfg, W0, 60, O.FIXED, dt)
+    W, _ = gpu_run(cfg, W0, 60, O.FIXED, dt)
+    assert np.array_equal(W, ref.W)
+
+
+def test_cfl1_translation_on_gpu():
+    """BASELINE pin on the GPU path: a=(1,0), C=1 -> exact roll after 100 steps."""
+    n = 64
+    cfg = O.Config(nx=n, ny=n, system=O.ADVECTION, param=(1.0, 0.0))
+    u0 = inputs.advection_dyadic(n, n, seed=0)
+    W, log = gpu_run(cfg, u0, 100, O.ADAPTIVE, 1.0)
+    assert np.all(log == 1.0 / n)
+    assert np.array_equal(W, np.roll(u0, 100, axis=1))
+
+
+@pytest.mark.parametrize("nslabs", [2, 4, 8])
+def test_decomposition_invariance_bitwise(nslabs):
+    """y-slab decomposition does not change a single bit."""
+    cfg = O.Config(nx=200, ny=256, system=O.EULER, param=(G,))
+    W0 = inputs.euler_random(200, 256, seed=3)
+    W1, l1 = gpu_run(cfg, W0, 30, O.ADAPTIVE, 0.45)
+    Wp, lp = gpu_run(cfg, W0, 30, O.ADAPTIVE, 0.45, nslabs=nslabs)
+    assert np.array_equal(l1, lp)
+    assert np.array_equal(W1, Wp)
+
+
+def test_decomposition_invariance_wall():
+    cfg = O.Config(nx=64, ny=128, system=O.EULER, param=(G,), bc_y=O.BC_WALL)
+    W0 = inputs.euler_random(64, 128, seed=4)
+    ref = O.run(cfg, W0, 20, O.ADAPTIVE, 0.45)
+    W, log = gpu_run(cfg, W0, 20, O.ADAPTIVE, 0.45, nslabs=4)
+    assert np.array_equal(log, ref.dt_log) and np.array_equal(W, ref.W)
+
+
+def test_naive_kernel_same_bits():
+    """The paper's one-thread-per-cell mapping gives the same bits."""
+    cfg, ic, C = CASES["euler_random_300x200"]
+    W0 = ic()
+    W1, l1 = gpu_run(cfg, W0, 20, O.ADAPTIVE, C)
+    W2, l2 = gpu_run(cfg, W0, 20, O.ADAPTIVE, C, flags=fv2d.FLAG_NAIVE)
+    assert np.array_equal(l1, l2) and np.array_equal(W1, W2)
+
+
+def test_soa_layout_roundtrip_and_step():
+    cfg, ic, C = CASES["euler_random_300x200"]
+    W0 = ic()
+    with solver_for(cfg) as s:
+        s.set_state(np.ascontiguousarray(W0.transpose(2, 0, 1)), fv2d.SOA)
+        assert np.array_equal(s.get_state(), W0)
+        s.step_adaptive(C, 5)
+        Wsoa = s.get_state(fv2d.SOA)
+    ref = O.run(cfg, W0, 5, O.ADAPTIVE, C)
+    assert np.array_equal(Wsoa.transpose(1, 2, 0), ref.W)
+
+
+def test_compute_and_check_dt():
+    cfg, ic, C = CASES["euler_laxliu3_256"]
+    W0 = ic()
+    s_ref, arg = O.smax(cfg, W0)
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        dt, smax = s.compute_dt(0.45)
+        assert smax == s_ref and dt == (0.45 * (1 / 256)) / s_ref
+        assert s.check_dt(dt) == s_ref
+        with pytest.raises(fv2d.FV2DError) as e:
+            s.check_dt(1.01 * (1 / 256) / s_ref)
+        assert e.value.code == fv2d.E_CFL
+
+
+def test_fixed_dt_cfl_violation_latched():
+    """P:149-151 / R14: a violation at step k leaves W^k readable, later steps are
+    no-ops; the error carries k and the argmax cell (lowest index on ties)."""
+    n = 64
+    cfg = O.Config(nx=n, ny=n, system=O.EULER, param=(G,))
+    W0 = inputs.euler_bell(n, n)
+    s0, arg0 = O.smax(cfg, W0)
+    bad_dt = (1 / n) / s0 * 1.0000001
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        s.step(bad_dt, 5)
+        with pytest.raises(fv2d.FV2DError) as e:
+            s.synchronize()
+        assert e.value.code == fv2d.E_CFL and e.value.step == 0 and e.value.cell == arg0
+        W = s.get_state(raise_on_error=False)
+        assert np.array_equal(W, W0)
+
+
+def test_nonfinite_detected():
+    n = 32
+    cfg = O.Config(nx=n, ny=n, system=O.EULER, param=(G,))
+    W0 = inputs.euler_random(n, n, seed=2)
+    W0[7, 9, 0] = -1.0                  # negative density
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        s.step(1e-4, 3)
+        with pytest.raises(fv2d.FV2DError) as e:
+            s.synchronize()
+        assert e.value.code == fv2d.E_NONFINITE and e.value.step == 0 and e.value.cell == 7 * n + 9
+        assert np.array_equal(s.get_state(raise_on_error=False), W0)
+
+
+# ---------------------------------------------------------------- spray (c4)
+def spray_case(n):
+    cfg = O.Config(nx=n, ny=n, system=O.SPRAY, param=(1.0, 1.0))
+    W0 = inputs.spray_taylor_green(n, n)
+    s0, _ = O.smax(cfg, W0)
+    return cfg, W0, 0.5 * (1.0 / n) / s0     # R17
+
+
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_SPLIT_SOURCE])
+def test_spray_per_step_and_trajectory(flags):
+    """Source parity is tolerance-only (GPU exp/sincospi vs glibc): per step
+    <= 1e-12 from the same W^k, after 20 steps <= 1e-10."""
+    cfg, W0, dt = spray_case(64)
+    ks = (0, 5, 19)
+    ref = O.run(cfg, W0, 20, O.FIXED, dt, dump_steps=ks + tuple(k + 1 for k in ks))
+    for k in ks:
+        W1, _ = gpu_run(cfg, ref.dumps[k], 1, O.FIXED, dt, flags=flags)
+        assert relerr(W1, ref.dumps[k + 1]) <= 1e-12
+    W, _ = gpu_run(cfg, W0, 20, O.FIXED, dt, flags=flags)
+    assert relerr(W, ref.W) <= 1e-10
+
+
+def test_spray_apply_source_standalone():
+    cfg, W0, dt = spray_case(48)
+    ref, _ = O.source_step(cfg, W0, 10 * dt)
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        s.apply_source(10 * dt)
+        W = s.get_state()
+    assert relerr(W, ref) <= 1e-12
+
+
+def test_spray_adaptive_fused():
+    cfg, W0, _ = spray_case(40)
+    ref = O.run(cfg, W0, 10, O.ADAPTIVE, 0.5)
+    W, log = gpu_run(cfg, W0, 10, O.ADAPTIVE, 0.5)
+    assert np.allclose(log, ref.dt_log, rtol=1e-12, atol=0)
+    assert relerr(W, ref.W) <= 1e-10
+
+
+# ---------------------------------------------------- full size, sampled (c3)
+def test_full_size_16384_sampled_rows():
+    """BASELINE configs[2] at full size (16384^2, Lax-Liu 3), in the launch
+    configuration bench.py times (fixed dt, fused kernel): one step, then
+    sampled row bands recomputed by the oracle (each cell's stencil is local:
+    a band [j0-1, j1+1) of W^n determines rows [j0, j1) of W^{n+1})."""
+    n = 16384
+    cfg = O.Config(nx=n, ny=n, system=O.EULER, param=(G,))
+    W0 = inputs.euler_lax_liu3(n, n)
+    dt = 0.45 * (1.0 / n) / 2.5
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        s.step(dt, 1)
+        W1 = s.get_state()
+    for j0 in (0, 4093, 8191, 16376):
+        lo, hi = j0 - 1, j0 + 9
+        rows = [r % n for r in range(lo, hi)]
+        band = W0[rows]
+        bcfg = O.Config(nx=n, ny=len(rows), system=O.EULER, param=(G,), y1=len(rows) / n)
+        out = O.transport_step(bcfg, band, dt)
+        assert np.array_equal(W1[[r % n for r in range(j0, j0 + 8)]], out[1:-1])
+    del W0, W1
