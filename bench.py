@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3_euler_16384", choices=sorted(WORKLOADS))
     ap.add_argument("--naive", action="store_true", help="paper's one-thread-per-cell kernel (baseline)")
+    ap.add_argument("--one-cell", action="store_true", help="one-cell-per-lane fused kernel (default: two)")
     ap.add_argument("--adaptive", action="store_true", help="adaptive dt (smax reduced in the epilogue)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -230,7 +231,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     stream = torch.cuda.current_stream()
-    flags = fv2d.FLAG_NAIVE if args.naive else 0
+    flags = (fv2d.FLAG_NAIVE if args.naive else 0) | (fv2d.FLAG_ONE_CELL if args.one_cell else 0)
     s = fv2d.Solver(nx, ny, fv2d.EULER, param=(GAMMA,), rank=rank, nranks=world, device=local, flags=flags,
                     nccl_id=nccl_id, stream=stream.cuda_stream)
     W0 = gen_ic(system, nx, ny, (rank * H, (rank + 1) * H))
@@ -310,7 +311,8 @@ def main():
         bpc = BYTES_PER_CELL[system]
         cells_per_launch = nx * H
         achieved = bpc * cells_per_launch / (kern_max * 1e-3) / 1e9
-        kernel = "fv_step_naive_kernel<Euler>" if args.naive else "fv_step_kernel<Euler,4,64>"
+        kernel = ("fv_step_naive_kernel<Euler>" if args.naive else
+                  "fv_step_kernel<Euler> (one cell/lane)" if args.one_cell else "fv_step_pair_kernel<Euler>")
         traffic = ncu_traffic(kernel)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -72,6 +72,8 @@ typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
                                         Same bits, ~2.5x the FP64 work; kept as a baseline. */
 #define FV2D_FLAG_SPLIT_SOURCE 0x2u /* spray: source as a separate pass after transport
                                         (default: fused into the transport pass, same math) */
+#define FV2D_FLAG_ONE_CELL 0x4u     /* fused kernel with one cell per lane instead of the
+                                        default two-cells-per-lane kernel (same bits) */
 
 typedef struct {
   int32_t nx, ny;          /* global mesh, >= 1; ny % (nranks*nslabs) == 0 */
@@ -165,11 +167,12 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt);
 /* Wait for all work of ctx; return the latched numerical error, if any. */
 fv2d_status fv2d_synchronize(fv2d_ctx* ctx);
 
-/* Zero-copy view of the current device state of local slab `slab`:
- * element (v, j, i) is at d_ptr[v*plane_stride + j*pitch + i], j in [0, ny_slab).
- * Valid until the next step. */
+/* Zero-copy view of the current device state of local slab `slab` (layout
+ * "row-interleaved SoA"): element (v, j, i) is at
+ * d_ptr[j*row_stride + v*pitch + i] for j in [-1, ny_slab] (rows -1 and ny_slab
+ * are the ghost rows).  Valid until the next step. */
 fv2d_status fv2d_device_state(fv2d_ctx* ctx, int32_t slab, double** d_ptr, int64_t* pitch,
-                              int64_t* plane_stride, int32_t* ny_slab);
+                              int64_t* row_stride, int32_t* ny_slab);
 
 /* Description of the last error: message (NUL-terminated, truncated to n), the
  * step index, the global cell index j*nx+i (lowest index among offending cells)

@@ -110,7 +110,6 @@ int nvar_of(int system) {
 }
 
 constexpr int kWarps = 4;
-constexpr int kRows = 64;
 
 }  // namespace
 
@@ -118,14 +117,12 @@ constexpr int kRows = 64;
 struct fv2d_ctx {
   fv2d_config cfg{};
   cudaStream_t stream = nullptr;
-  int nv = 0, nx = 0, H = 0, pitch = 0, nslabs = 1, G = 1;
-  long long plane = 0;
+  int nv = 0, nx = 0, H = 0, pitch = 0, nslabs = 1, G = 1, rps = 64;
+  long long rs = 0;  // row stride (nv * pitch); a buffer holds rows -1..H
   double dx = 0, dy = 0, hmin = 0;
-  // per local slab
+  // per local slab: two ping-pong buffers of (H+2) rows (ghost rows -1 and H inside)
   double* buf[kMaxSlabs][2] = {};
-  double* gs[kMaxSlabs][2] = {};
-  double* gn[kMaxSlabs][2] = {};
-  double* send_s = nullptr;  // nranks > 1: packed boundary rows to send
+  double* send_s = nullptr;  // nranks > 1: boundary rows to send
   double* send_n = nullptr;
   double* staging = nullptr;
   size_t staging_bytes = 0;
@@ -190,7 +187,11 @@ fv2d_status set_err(fv2d_ctx* c, fv2d_status st, const char* fmt, ...) {
     if (e_ != cudaSuccess) return set_err(ctx, FV2D_E_CUDA, "launch failed: %s", cudaGetErrorString(e_)); \
   } while (0)
 
-// Ghost targets of local slab s for writes landing in ghost buffers of parity q.
+double* row_ptr(const fv2d_ctx* ctx, int s, int p, int j) { return ctx->buf[s][p] + (long long)(j + 1) * ctx->rs; }
+double* ghost_s(const fv2d_ctx* ctx, int s, int p) { return row_ptr(ctx, s, p, -1); }
+double* ghost_n(const fv2d_ctx* ctx, int s, int p) { return row_ptr(ctx, s, p, ctx->H); }
+
+// Ghost targets of local slab s for writes landing in ghost rows of parity q.
 void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   const int g = ctx->cfg.rank * ctx->nslabs + s;
   const int G = ctx->G;
@@ -200,22 +201,22 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   d.dst_n = nullptr;
   d.mirror_s = -1;
   d.mirror_n = -1;
-  // south boundary row (row 0) -> south neighbour's north ghost
+  // south boundary row (row 0) -> south neighbour's north ghost row (row H)
   if (g > 0 || per) {
     const int gs_ = (g - 1 + G) % G;
-    if (gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ctx->gn[gs_ % ctx->nslabs][q];
+    if (gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ghost_n(ctx, gs_ % ctx->nslabs, q);
     else d.dst_s = ctx->send_s;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
-    d.dst_s = ctx->gs[s][q];
+    d.dst_s = ghost_s(ctx, s, q);
     d.mirror_s = my_y;
   }
-  // north boundary row (row H-1) -> north neighbour's south ghost
+  // north boundary row (row H-1) -> north neighbour's south ghost row (row -1)
   if (g < G - 1 || per) {
     const int gn_ = (g + 1) % G;
-    if (gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ctx->gs[gn_ % ctx->nslabs][q];
+    if (gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ghost_s(ctx, gn_ % ctx->nslabs, q);
     else d.dst_n = ctx->send_n;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
-    d.dst_n = ctx->gn[s][q];
+    d.dst_n = ghost_n(ctx, s, q);
     d.mirror_n = my_y;
   }
 }
@@ -228,17 +229,16 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.nslabs = ctx->nslabs;
   for (int s = 0; s < ctx->nslabs; ++s) {
     SlabDesc& d = a.slab[s];
-    d.in = ctx->buf[s][p];
-    d.out = ctx->buf[s][q];
-    d.gs = ctx->gs[s][p];
-    d.gn = ctx->gn[s][p];
+    d.in = row_ptr(ctx, s, p, 0);
+    d.out = row_ptr(ctx, s, q, 0);
     ghost_targets(ctx, s, q, d);
     d.row0 = (ctx->cfg.rank * ctx->nslabs + s) * ctx->H;
     d.H = ctx->H;
   }
   a.nx = ctx->nx;
   a.pitch = ctx->pitch;
-  a.plane = ctx->plane;
+  a.rs = ctx->rs;
+  a.rows_per_strip = ctx->rps;
   a.bcx = ctx->cfg.bc_x;
   for (int v = 0; v < kMaxVar; ++v) a.dirx[v] = ctx->cfg.dirichlet[v];
   a.dx = ctx->dx;
@@ -285,9 +285,31 @@ struct LaunchStep {
       dim3 grid((ctx->nx + 31) / 32, (ctx->H + 7) / 8, ctx->nslabs);
       fv_step_naive_kernel<Sys><<<grid, 256, 0, ctx->stream>>>(a);
     } else {
-      const int cols = 30 * kWarps;
-      dim3 grid((ctx->nx + cols - 1) / cols, (ctx->H + kRows - 1) / kRows, ctx->nslabs);
-      fv_step_kernel<Sys, kWarps, kRows><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+      constexpr int D = 4;
+      const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC;
+      // spray (nVar 6) uses the one-cell kernel: its fused source needs the registers
+      if constexpr (Sys::NV == 6) {
+        const int cols = 30 * kWarps;
+        dim3 grid((ctx->nx + cols - 1) / cols, (ctx->H + ctx->rps - 1) / ctx->rps, ctx->nslabs);
+        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+      } else if (ctx->cfg.flags & FV2D_FLAG_ONE_CELL) {
+        const int cols = 30 * kWarps;
+        dim3 grid((ctx->nx + cols - 1) / cols, (ctx->H + ctx->rps - 1) / ctx->rps, ctx->nslabs);
+        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+      } else {
+        const int warps = (ctx->nx + 1 + 61) / 62;
+        dim3 grid((warps + kWarps - 1) / kWarps, (ctx->H + ctx->rps - 1) / ctx->rps, ctx->nslabs);
+        if (xper && !a.adaptive) fv_step_pair_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (xper && a.adaptive) fv_step_pair_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (!xper && !a.adaptive) fv_step_pair_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        if (!xper && a.adaptive) fv_step_pair_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+      }
     }
   }
 };
@@ -318,12 +340,12 @@ fv2d_status exchange(fv2d_ctx* ctx, int q) {
   const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
   const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
   const bool has_s = r > 0 || per, has_n = r < P - 1 || per;
-  const size_t cnt = (size_t)ctx->nv * ctx->pitch;
+  const size_t cnt = (size_t)ctx->rs;  // one whole cell row: nv variable rows
   CKN(g_nccl.GroupStart());
   if (has_s) CKN(g_nccl.Send(ctx->send_s, cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, ctx->stream));
-  if (has_n) CKN(g_nccl.Recv(ctx->gn[0][q], cnt, ncclFloat64, (r + 1) % P, ctx->comm, ctx->stream));
+  if (has_n) CKN(g_nccl.Recv(ghost_n(ctx, 0, q), cnt, ncclFloat64, (r + 1) % P, ctx->comm, ctx->stream));
   if (has_n) CKN(g_nccl.Send(ctx->send_n, cnt, ncclFloat64, (r + 1) % P, ctx->comm, ctx->stream));
-  if (has_s) CKN(g_nccl.Recv(ctx->gs[0][q], cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, ctx->stream));
+  if (has_s) CKN(g_nccl.Recv(ghost_s(ctx, 0, q), cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, ctx->stream));
   CKN(g_nccl.GroupEnd());
   return FV2D_OK;
 }
@@ -476,11 +498,8 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   cudaSetDevice(ctx->cfg.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (int s = 0; s < kMaxSlabs; ++s)
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < 2; ++p)
       if (ctx->buf[s][p]) cudaFree(ctx->buf[s][p]);
-      if (ctx->gs[s][p]) cudaFree(ctx->gs[s][p]);
-      if (ctx->gn[s][p]) cudaFree(ctx->gn[s][p]);
-    }
   if (ctx->send_s) cudaFree(ctx->send_s);
   if (ctx->send_n) cudaFree(ctx->send_n);
   if (ctx->staging) cudaFree(ctx->staging);
@@ -522,7 +541,13 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   ctx->nx = c.nx;
   ctx->H = (int)H;
   ctx->pitch = (c.nx + 31) / 32 * 32;
-  ctx->plane = (long long)ctx->pitch * H;
+  ctx->rs = (long long)ctx->pitch * nv;
+  {
+    // strip height of the marching kernel: enough CTAs for ~8 per SM, 16..128 rows
+    const long long colblocks = ((c.nx + 62) / 62 + kWarps - 1) / kWarps;
+    long long rps = colblocks * H / (148 * 8);
+    ctx->rps = (int)std::max<long long>(16, std::min<long long>(128, rps));
+  }
   ctx->nslabs = c.nslabs;
   ctx->G = c.nranks * c.nslabs;
   ctx->dx = (c.x1 - c.x0) / c.nx;
@@ -544,16 +569,12 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     }                                                                                              \
   } while (0)
   CKC(cudaSetDevice(c.device));
-  const size_t state_bytes = (size_t)nv * ctx->plane * sizeof(double);
-  const size_t row_bytes = (size_t)nv * ctx->pitch * sizeof(double);
+  const size_t state_bytes = ((size_t)(H + 2) * ctx->rs + 64) * sizeof(double);
+  const size_t row_bytes = (size_t)ctx->rs * sizeof(double);
   for (int s = 0; s < ctx->nslabs; ++s)
     for (int p = 0; p < 2; ++p) {
       CKC(cudaMalloc(&ctx->buf[s][p], state_bytes));
       CKC(cudaMemset(ctx->buf[s][p], 0, state_bytes));
-      CKC(cudaMalloc(&ctx->gs[s][p], row_bytes));
-      CKC(cudaMalloc(&ctx->gn[s][p], row_bytes));
-      CKC(cudaMemset(ctx->gs[s][p], 0, row_bytes));
-      CKC(cudaMemset(ctx->gn[s][p], 0, row_bytes));
     }
   if (c.nranks > 1) {
     CKC(cudaMalloc(&ctx->send_s, row_bytes));
@@ -591,11 +612,11 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
       const int g = c.rank * c.nslabs + s;
       for (int p = 0; p < 2; ++p) {
         if (g == 0)
-          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ctx->gs[s][p], nv, c.nx, ctx->pitch, c.dirichlet[0],
+          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ghost_s(ctx, s, p), nv, c.nx, ctx->pitch, c.dirichlet[0],
                                                              c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
                                                              c.dirichlet[4], c.dirichlet[5]);
         if (g == ctx->G - 1)
-          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ctx->gn[s][p], nv, c.nx, ctx->pitch, c.dirichlet[0],
+          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ghost_n(ctx, s, p), nv, c.nx, ctx->pitch, c.dirichlet[0],
                                                              c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
                                                              c.dirichlet[4], c.dirichlet[5]);
       }
@@ -617,7 +638,7 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   // ghost rows of parity 0 from the new W^0, then reset the counters
   ctx->steps = 0;
   StepArgs a = make_args(ctx, 1);  // "reading" parity 1 means ghost targets of parity 0
-  for (int s = 0; s < ctx->nslabs; ++s) a.slab[s].in = ctx->buf[s][0];
+  for (int s = 0; s < ctx->nslabs; ++s) a.slab[s].in = row_ptr(ctx, s, 0, 0);
   fill_halo_kernel<<<dim3((ctx->nx + 127) / 128, 1, ctx->nslabs), 128, 0, ctx->stream>>>(a, ctx->nv);
   CKL();
   fv2d_status st = exchange(ctx, 0);
@@ -652,7 +673,7 @@ static fv2d_status upload(fv2d_ctx* ctx, const double* src, fv2d_layout layout, 
     const long long nyl = (long long)H * ctx->nslabs;
     for (int s = 0; s < ctx->nslabs; ++s)
       for (int v = 0; v < nv; ++v)
-        CK(cudaMemcpy2DAsync(ctx->buf[s][0] + v * ctx->plane, ctx->pitch * sizeof(double),
+        CK(cudaMemcpy2DAsync(row_ptr(ctx, s, 0, 0) + v * ctx->pitch, ctx->rs * sizeof(double),
                              src + (size_t)v * nyl * nx + (size_t)s * H * nx, nx * sizeof(double),
                              nx * sizeof(double), H, kind, ctx->stream));
   } else {
@@ -661,8 +682,8 @@ static fv2d_status upload(fv2d_ctx* ctx, const double* src, fv2d_layout layout, 
     const size_t bytes = (size_t)nv * nx * H * ctx->nslabs * sizeof(double);
     CK(cudaMemcpyAsync(ctx->staging, src, bytes, kind, ctx->stream));
     for (int s = 0; s < ctx->nslabs; ++s) {
-      aos_to_soa_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->staging + (size_t)s * H * nx * nv, ctx->buf[s][0], nv,
-                                                          nx, H, ctx->pitch, ctx->plane);
+      aos_to_dev_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->staging + (size_t)s * H * nx * nv,
+                                                          row_ptr(ctx, s, 0, 0), nv, nx, H, ctx->pitch, ctx->rs);
       CKL();
     }
   }
@@ -693,14 +714,15 @@ fv2d_status fv2d_get_state(fv2d_ctx* ctx, double* host, fv2d_layout layout) {
     for (int s = 0; s < ctx->nslabs; ++s)
       for (int v = 0; v < nv; ++v)
         CK(cudaMemcpy2DAsync(host + (size_t)v * nyl * nx + (size_t)s * H * nx, nx * sizeof(double),
-                             ctx->buf[s][p] + v * ctx->plane, ctx->pitch * sizeof(double), nx * sizeof(double), H,
-                             cudaMemcpyDeviceToHost, ctx->stream));
+                             row_ptr(ctx, s, p, 0) + v * ctx->pitch, ctx->rs * sizeof(double), nx * sizeof(double),
+                             H, cudaMemcpyDeviceToHost, ctx->stream));
   } else {
     fv2d_status s1 = ensure_staging(ctx);
     if (s1) return s1;
     for (int s = 0; s < ctx->nslabs; ++s) {
-      soa_to_aos_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->buf[s][p], ctx->staging + (size_t)s * H * nx * nv, nv,
-                                                          nx, H, ctx->pitch, ctx->plane);
+      dev_to_aos_kernel<<<148 * 8, 256, 0, ctx->stream>>>(row_ptr(ctx, s, p, 0),
+                                                          ctx->staging + (size_t)s * H * nx * nv, nv, nx, H,
+                                                          ctx->pitch, ctx->rs);
       CKL();
     }
     CK(cudaMemcpyAsync(host, ctx->staging, (size_t)nv * nx * H * ctx->nslabs * sizeof(double),
@@ -805,7 +827,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
     if (ctx->profiling) CK(cudaEventRecord(e1, ctx->stream));
     if (split) {
       StepArgs b = a;
-      for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = ctx->buf[s][1 - p];
+      for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, 1 - p, 0);
       dim3 grid((ctx->nx + 127) / 128, ctx->H, ctx->nslabs);
       spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt);
       CKL();
@@ -865,7 +887,7 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   const int p = cur_parity(ctx);
   // in place on parity p: halo targets are the ghost buffers of parity p
   StepArgs b = make_args(ctx, 1 - p);
-  for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = ctx->buf[s][p];
+  for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, p, 0);
   b.step = ctx->steps;
   dim3 grid((ctx->nx + 127) / 128, ctx->H, ctx->nslabs);
   spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt);
@@ -887,12 +909,12 @@ fv2d_status fv2d_synchronize(fv2d_ctx* ctx) {
   return report(ctx, st);
 }
 
-fv2d_status fv2d_device_state(fv2d_ctx* ctx, int32_t slab, double** d_ptr, int64_t* pitch, int64_t* plane_stride,
+fv2d_status fv2d_device_state(fv2d_ctx* ctx, int32_t slab, double** d_ptr, int64_t* pitch, int64_t* row_stride,
                               int32_t* ny_slab) {
   if (!ctx || slab < 0 || slab >= ctx->nslabs) return FV2D_E_ARG;
-  if (d_ptr) *d_ptr = ctx->buf[slab][cur_parity(ctx)];
+  if (d_ptr) *d_ptr = row_ptr(ctx, slab, cur_parity(ctx), 0);
   if (pitch) *pitch = ctx->pitch;
-  if (plane_stride) *plane_stride = ctx->plane;
+  if (row_stride) *row_stride = ctx->rs;
   if (ny_slab) *ny_slab = ctx->H;
   return FV2D_OK;
 }

@@ -18,7 +18,7 @@ OK, E_ARG, E_CFL, E_NONFINITE, E_RECON, E_CUDA, E_NCCL, E_STATE = range(8)
 ADVECTION, EULER, SPRAY = 0, 1, 2
 BC_PERIODIC, BC_DIRICHLET, BC_WALL = 0, 1, 2
 AOS, SOA = 0, 1
-FLAG_NAIVE, FLAG_SPLIT_SOURCE = 0x1, 0x2
+FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL = 0x1, 0x2, 0x4
 NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
 _NAMES = {OK: "OK", E_ARG: "E_ARG", E_CFL: "E_CFL", E_NONFINITE: "E_NONFINITE", E_RECON: "E_RECON",
           E_CUDA: "E_CUDA", E_NCCL: "E_NCCL", E_STATE: "E_STATE"}

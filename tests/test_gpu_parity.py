@@ -266,3 +266,29 @@ def test_full_size_16384_sampled_rows():
         out = O.transport_step(bcfg, band, dt)
         assert np.array_equal(W1[[r % n for r in range(j0, j0 + 8)]], out[1:-1])
     del W0, W1
+
+
+@pytest.mark.parametrize("name", ["euler_random_300x200", "euler_sod_wall_x_250x40", "euler_dirichlet_130x70",
+                                  "adv_dyadic_64"])
+def test_one_cell_and_pair_kernels_same_bits(name):
+    """Both fused variants (one and two cells per lane) and the naive kernel agree bitwise."""
+    cfg, ic, C = CASES[name]
+    W0 = ic()
+    W1, l1 = gpu_run(cfg, W0, 25, O.ADAPTIVE, C)
+    W2, l2 = gpu_run(cfg, W0, 25, O.ADAPTIVE, C, flags=fv2d.FLAG_ONE_CELL)
+    W3, l3 = gpu_run(cfg, W0, 25, O.ADAPTIVE, C, flags=fv2d.FLAG_NAIVE)
+    assert np.array_equal(l1, l2) and np.array_equal(l1, l3)
+    assert np.array_equal(W1, W2) and np.array_equal(W1, W3)
+
+
+@pytest.mark.parametrize("nx", [61, 62, 63, 64, 123, 124, 125, 249, 250, 251, 497])
+def test_ragged_widths_periodic_and_wall(nx):
+    """Warp/CTA tiling edges: widths around multiples of 62/124/248 columns, odd and
+    even (odd nx forces the split 8-byte copy path at the periodic seam)."""
+    ny = 20
+    for bc in (O.BC_PERIODIC, O.BC_WALL):
+        cfg = O.Config(nx=nx, ny=ny, system=O.EULER, param=(G,), bc_x=bc, x1=nx / 64)
+        W0 = inputs.euler_random(nx, ny, seed=nx)
+        ref = O.run(cfg, W0, 5, O.ADAPTIVE, 0.45)
+        W, log = gpu_run(cfg, W0, 5, O.ADAPTIVE, 0.45)
+        assert np.array_equal(log, ref.dt_log) and np.array_equal(W, ref.W)
