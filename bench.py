@@ -213,6 +213,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_1701_05431_b200 import dist as D
     from paper_1701_05431_b200 import fv2d
 
     torch.cuda.set_device(local)
@@ -224,17 +225,16 @@ def main():
     ny = ny_global * world if weak else ny_global
     if ny % world:
         raise SystemExit(f"ny={ny} not divisible by {world}")
-    H = ny // world
+    j0, j1 = D.slab_rows(rank, world, ny)
+    H = j1 - j0
     nccl_id = None
     if world > 1:
-        obj = [fv2d.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = D.broadcast_bytes(fv2d.nccl_unique_id() if rank == 0 else None)
     stream = torch.cuda.current_stream()
     flags = (fv2d.FLAG_NAIVE if args.naive else 0) | (fv2d.FLAG_ONE_CELL if args.one_cell else 0)
     s = fv2d.Solver(nx, ny, fv2d.EULER, param=(GAMMA,), rank=rank, nranks=world, device=local, flags=flags,
                     nccl_id=nccl_id, stream=stream.cuda_stream)
-    W0 = gen_ic(system, nx, ny, (rank * H, (rank + 1) * H))
+    W0 = gen_ic(system, nx, ny, (j0, j1))
     s.set_state(W0)
     dt, smax0 = s.compute_dt(CFL)    # the paper's constant dt, set at start
 
@@ -269,10 +269,7 @@ def main():
     s.synchronize()                      # no latched CFL/non-finite error in the timed steps
     kern_ms = st1["step_kernel_ms"] / max(1, st1["step_kernels_timed"])
     launches = st1["kernel_launches"] - st0["kernel_launches"]
-    t = torch.tensor([ms, kern_ms], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, kern_max = float(t[0]), float(t[1])
+    ms_max, kern_max = D.max_over_ranks([ms, kern_ms], device="cuda")
     cells_total = nx * ny
     value = cells_total * args.steps / (ms_max * 1e-3)
 
@@ -293,11 +290,9 @@ def main():
             s.get_state_ptr(ptr)          # D2H of the step's result
         e1.record(stream)
         barrier()
-        et = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        (et,) = D.max_over_ranks([e0.elapsed_time(e1)], device="cuda")
         nbytes = W0.size * 8
-        e2e = {"value": cells_total * args.e2e_steps / (float(et[0]) * 1e-3), "unit": UNIT,
+        e2e = {"value": cells_total * args.e2e_steps / (et * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
                "api": "fv2d_set_state(host AoS, pinned) + fv2d_step + fv2d_get_state(host AoS)"}
         del hostbuf

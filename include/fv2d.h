@@ -71,9 +71,16 @@ typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
                                         every neighbour re-derived, every face computed twice.
                                         Same bits, ~2.5x the FP64 work; kept as a baseline. */
 #define FV2D_FLAG_SPLIT_SOURCE 0x2u /* spray: source as a separate pass after transport
-                                        (default: fused into the transport pass, same math) */
+                                        (the default; kept for compatibility) */
 #define FV2D_FLAG_ONE_CELL 0x4u     /* fused kernel with one cell per lane instead of the
                                         default two-cells-per-lane kernel (same bits) */
+#define FV2D_FLAG_FUSE_SOURCE 0x10u /* spray: apply the source in the transport pass's
+                                        epilogue (one pass, 96 B/cell less traffic; lower
+                                        occupancy for the FP64-bound Newton, slower on B200) */
+#define FV2D_FLAG_NCCL_LOOPBACK 0x8u /* take the NCCL halo/all-reduce path even with
+                                        nranks == 1 (self send/recv; needs an id from
+                                        fv2d_nccl_unique_id); exercises the multi-GPU
+                                        plumbing on one device */
 
 typedef struct {
   int32_t nx, ny;          /* global mesh, >= 1; ny % (nranks*nslabs) == 0 */

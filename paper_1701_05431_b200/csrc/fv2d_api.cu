@@ -135,6 +135,7 @@ struct fv2d_ctx {
   unsigned long long* newton = nullptr;
   double* trig = nullptr;  // sx[nx] cx[nx] sy[ny] cy[ny]
   ncclComm_t comm = nullptr;
+  bool use_nccl = false;  // nranks > 1, or FV2D_FLAG_NCCL_LOOPBACK (self exchange on 1 rank)
   // host state
   bool has_state = false;
   bool dt_valid = false;
@@ -204,7 +205,7 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   // south boundary row (row 0) -> south neighbour's north ghost row (row H)
   if (g > 0 || per) {
     const int gs_ = (g - 1 + G) % G;
-    if (gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ghost_n(ctx, gs_ % ctx->nslabs, q);
+    if (!ctx->use_nccl && gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ghost_n(ctx, gs_ % ctx->nslabs, q);
     else d.dst_s = ctx->send_s;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
     d.dst_s = ghost_s(ctx, s, q);
@@ -213,7 +214,7 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   // north boundary row (row H-1) -> north neighbour's south ghost row (row -1)
   if (g < G - 1 || per) {
     const int gn_ = (g + 1) % G;
-    if (gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ghost_s(ctx, gn_ % ctx->nslabs, q);
+    if (!ctx->use_nccl && gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ghost_s(ctx, gn_ % ctx->nslabs, q);
     else d.dst_n = ctx->send_n;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
     d.dst_n = ghost_n(ctx, s, q);
@@ -256,8 +257,8 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.status = ctx->dscal + 2;
   a.bad_cell = ctx->dscal + 3;
   a.done = ctx->done;
-  a.fused_finalize = ctx->cfg.nranks == 1 ? 1 : 0;
-  a.fuse_source = (ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_SPLIT_SOURCE)) ? 1 : 0;
+  a.fused_finalize = ctx->use_nccl ? 0 : 1;
+  a.fuse_source = (ctx->cfg.system == FV2D_SPRAY && (ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE)) ? 1 : 0;
   if (ctx->trig) {
     a.sx_tab = ctx->trig;
     a.cx_tab = ctx->trig + ctx->nx;
@@ -336,7 +337,7 @@ int cur_parity(const fv2d_ctx* ctx) { return (int)(ctx->steps & 1); }
 
 // NCCL halo exchange into ghost buffers of parity q, from send_s/send_n.
 fv2d_status exchange(fv2d_ctx* ctx, int q) {
-  if (ctx->cfg.nranks == 1) return FV2D_OK;
+  if (!ctx->use_nccl) return FV2D_OK;
   const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
   const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
   const bool has_s = r > 0 || per, has_n = r < P - 1 || per;
@@ -390,7 +391,7 @@ fv2d_status reduce_current(fv2d_ctx* ctx, double* smax_out, unsigned long long* 
   dispatch<LaunchReduce>(ctx->cfg.system, ctx, a);
   CKL();
   unsigned long long h[2];
-  if (ctx->cfg.nranks > 1) {
+  if (ctx->use_nccl) {
     fv2d_status s = allreduce_scalars(ctx);
     if (s) return s;
     CK(cudaMemcpyAsync(h, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
@@ -521,7 +522,7 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   const fv2d_config& c = *cfg_in;
   const int nv = nvar_of(c.system);
   if (nv < 0 || c.nvar != nv || c.nx < 1 || c.ny < 1 || c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks ||
-      c.nslabs < 1 || c.nslabs > kMaxSlabs || (c.nranks > 1 && c.nslabs != 1) ||
+      c.nslabs < 1 || c.nslabs > kMaxSlabs || ((c.nranks > 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK)) && c.nslabs != 1) ||
       c.ny % (c.nranks * c.nslabs) != 0 || !(c.x1 > c.x0) || !(c.y1 > c.y0) || c.bc_x < 0 || c.bc_x > 2 ||
       c.bc_y < 0 || c.bc_y > 2)
     return FV2D_E_ARG;
@@ -532,10 +533,12 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     if (c.reserved[k] != 0) return FV2D_E_ARG;
   const long long H = c.ny / (c.nranks * c.nslabs);
   if (H < 1) return FV2D_E_ARG;
-  if (c.nranks > 1 && (!nccl_id || !load_nccl())) return FV2D_E_NCCL;
+  const bool use_nccl = c.nranks > 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK);
+  if (use_nccl && (!nccl_id || !load_nccl())) return FV2D_E_NCCL;
 
   fv2d_ctx* ctx = new fv2d_ctx();
   ctx->cfg = c;
+  ctx->use_nccl = use_nccl;
   ctx->stream = (cudaStream_t)cuda_stream;
   ctx->nv = nv;
   ctx->nx = c.nx;
@@ -543,10 +546,12 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   ctx->pitch = (c.nx + 31) / 32 * 32;
   ctx->rs = (long long)ctx->pitch * nv;
   {
-    // strip height of the marching kernel: enough CTAs for ~8 per SM, 16..128 rows
+    // strip height of the marching kernel: ~2 waves of 3 CTAs per SM for large
+    // grids (128 rows: 1.6% halo-row overhead), down to 4 rows for small grids
+    // where latency, not bandwidth, bounds the step
     const long long colblocks = ((c.nx + 62) / 62 + kWarps - 1) / kWarps;
-    long long rps = colblocks * H / (148 * 8);
-    ctx->rps = (int)std::max<long long>(16, std::min<long long>(128, rps));
+    long long rps = colblocks * H / (148 * 6);
+    ctx->rps = (int)std::max<long long>(4, std::min<long long>(128, rps));
   }
   ctx->nslabs = c.nslabs;
   ctx->G = c.nranks * c.nslabs;
@@ -576,7 +581,7 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
       CKC(cudaMalloc(&ctx->buf[s][p], state_bytes));
       CKC(cudaMemset(ctx->buf[s][p], 0, state_bytes));
     }
-  if (c.nranks > 1) {
+  if (use_nccl) {
     CKC(cudaMalloc(&ctx->send_s, row_bytes));
     CKC(cudaMalloc(&ctx->send_n, row_bytes));
     CKC(cudaMemset(ctx->send_s, 0, row_bytes));
@@ -624,7 +629,7 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     CKC(cudaGetLastError());
   }
   CKC(cudaDeviceSynchronize());
-  if (c.nranks > 1) {
+  if (use_nccl) {
     ncclUniqueId u;
     memcpy(&u, nccl_id, sizeof u);
     if (g_nccl.CommInitRank(&ctx->comm, c.nranks, u, c.rank) != ncclSuccess) return fail(FV2D_E_NCCL);
@@ -803,10 +808,18 @@ static fv2d_status prof_events(fv2d_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1) 
   return FV2D_OK;
 }
 
+// The split source pass of a step: dt is the fixed dt or, in adaptive mode,
+// the device scalar (read inside the kernel so the launch stays asynchronous).
+static void spray_source_dt_kernel_launch(fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
+  StepArgs b = a;
+  for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, 1 - (int)(ctx->steps & 1), 0);
+  spray_source_step_kernel<<<grid, 128, 0, ctx->stream>>>(b);
+}
+
 static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double cfl, int32_t nsteps) {
   fv2d_status st = ensure_dt_log(ctx, ctx->steps + nsteps);
   if (st) return st;
-  const bool split = ctx->cfg.system == FV2D_SPRAY && (ctx->cfg.flags & FV2D_FLAG_SPLIT_SOURCE);
+  const bool split = ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE);
   for (int32_t k = 0; k < nsteps; ++k) {
     const int p = cur_parity(ctx);
     StepArgs a = make_args(ctx, p);
@@ -814,25 +827,30 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
     a.dt = dt;
     a.cfl = cfl;
     a.step = ctx->steps;
-    if (split || ctx->cfg.nranks > 1) a.fused_finalize = 0;
-    if (split) a.fuse_source = 0;
+    if (ctx->use_nccl) a.fused_finalize = 0;
+    StepArgs at = a;  // transport pass
+    if (split) {
+      at.fuse_source = 0;
+      at.fused_finalize = 0;  // the source pass ends the step
+      at.no_smax = 1;         // adaptive: smax of the post-source state comes from the source pass
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->profiling) {
       st = prof_events(ctx, &e0, &e1);
       if (st) return st;
       CK(cudaEventRecord(e0, ctx->stream));
     }
-    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, a);
+    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, at);
     CKL();
     if (ctx->profiling) CK(cudaEventRecord(e1, ctx->stream));
     if (split) {
-      StepArgs b = a;
-      for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, 1 - p, 0);
-      dim3 grid((ctx->nx + 127) / 128, ctx->H, ctx->nslabs);
-      spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt);
+      // in place on the transport output; dt: the fixed dt, or read from the
+      // device in adaptive mode (the finalize writes dt_{n+1} only after this pass)
+      dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
+      spray_source_dt_kernel_launch(ctx, a, grid);
       CKL();
     }
-    if (ctx->cfg.nranks > 1) {
+    if (ctx->use_nccl) {
       st = exchange(ctx, 1 - p);
       if (st) return st;
       st = allreduce_scalars(ctx);
@@ -858,8 +876,6 @@ fv2d_status fv2d_step(fv2d_ctx* ctx, double dt, int32_t nsteps) {
 fv2d_status fv2d_step_adaptive(fv2d_ctx* ctx, double cfl, int32_t nsteps, double* dt_log) {
   if (!ctx || !(cfl > 0.0) || !(cfl <= 1.0) || nsteps < 0) return FV2D_E_ARG;
   if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
-  if (ctx->cfg.system == FV2D_SPRAY && (ctx->cfg.flags & FV2D_FLAG_SPLIT_SOURCE))
-    return set_err(ctx, FV2D_E_ARG, "adaptive dt needs the fused spray source (smax of the post-source state)");
   CK(cudaSetDevice(ctx->cfg.device));
   if (!ctx->dt_valid) {
     double d, s;
@@ -889,8 +905,8 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   StepArgs b = make_args(ctx, 1 - p);
   for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, p, 0);
   b.step = ctx->steps;
-  dim3 grid((ctx->nx + 127) / 128, ctx->H, ctx->nslabs);
-  spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt);
+  dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
+  spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt, 0);
   CKL();
   fv2d_status st = exchange(ctx, p);
   if (st) return st;

@@ -18,7 +18,7 @@ OK, E_ARG, E_CFL, E_NONFINITE, E_RECON, E_CUDA, E_NCCL, E_STATE = range(8)
 ADVECTION, EULER, SPRAY = 0, 1, 2
 BC_PERIODIC, BC_DIRICHLET, BC_WALL = 0, 1, 2
 AOS, SOA = 0, 1
-FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL = 0x1, 0x2, 0x4
+FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL, FLAG_NCCL_LOOPBACK, FLAG_FUSE_SOURCE = 0x1, 0x2, 0x4, 0x8, 0x10
 NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
 _NAMES = {OK: "OK", E_ARG: "E_ARG", E_CFL: "E_CFL", E_NONFINITE: "E_NONFINITE", E_RECON: "E_RECON",
           E_CUDA: "E_CUDA", E_NCCL: "E_NCCL", E_STATE: "E_STATE"}
@@ -88,7 +88,21 @@ class FV2DError(RuntimeError):
         self.code, self.message, self.step, self.cell, self.value = code, message, step, cell, value
 
 
+def _preload_nccl():
+    """Load torch's NCCL (the nvidia-nccl wheel) globally first, so the library's
+    dlopen("libnccl.so.2") resolves to the same single copy torch uses."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        path = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            C.CDLL(path, mode=C.RTLD_GLOBAL)
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _preload_nccl()
     buf = C.create_string_buffer(128)
     rc = lib().fv2d_nccl_unique_id(buf)
     if rc != OK:
@@ -124,6 +138,8 @@ class Solver:
         self.cfg = cfg
         self.nx, self.ny, self.nv, self.system = nx, ny, NVAR[system], system
         self.ny_local = ny // nranks
+        if nranks > 1 or (flags & FLAG_NCCL_LOOPBACK):
+            _preload_nccl()
         h = C.c_void_p()
         rc = L.fv2d_create(C.byref(cfg), nccl_id, C.c_void_p(stream or 0), C.byref(h))
         if rc != OK:

@@ -212,7 +212,7 @@ def spray_case(n):
     return cfg, W0, 0.5 * (1.0 / n) / s0     # R17
 
 
-@pytest.mark.parametrize("flags", [0, fv2d.FLAG_SPLIT_SOURCE])
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_FUSE_SOURCE])
 def test_spray_per_step_and_trajectory(flags):
     """Source parity is tolerance-only (GPU exp/sincospi vs glibc): per step
     <= 1e-12 from the same W^k, after 20 steps <= 1e-10."""
@@ -236,10 +236,13 @@ def test_spray_apply_source_standalone():
     assert relerr(W, ref) <= 1e-12
 
 
-def test_spray_adaptive_fused():
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_FUSE_SOURCE])
+def test_spray_adaptive(flags):
+    """Adaptive dt with the source: smax is reduced on the post-source state
+    (split: in the source pass's epilogue; fused: in the step epilogue)."""
     cfg, W0, _ = spray_case(40)
     ref = O.run(cfg, W0, 10, O.ADAPTIVE, 0.5)
-    W, log = gpu_run(cfg, W0, 10, O.ADAPTIVE, 0.5)
+    W, log = gpu_run(cfg, W0, 10, O.ADAPTIVE, 0.5, flags=flags)
     assert np.allclose(log, ref.dt_log, rtol=1e-12, atol=0)
     assert relerr(W, ref.W) <= 1e-10
 
@@ -292,3 +295,35 @@ def test_ragged_widths_periodic_and_wall(nx):
         ref = O.run(cfg, W0, 5, O.ADAPTIVE, 0.45)
         W, log = gpu_run(cfg, W0, 5, O.ADAPTIVE, 0.45)
         assert np.array_equal(log, ref.dt_log) and np.array_equal(W, ref.W)
+
+
+@pytest.mark.parametrize("bc_y", [O.BC_PERIODIC, O.BC_WALL])
+def test_nccl_loopback_path_bitwise(bc_y):
+    """The multi-GPU plumbing (boundary rows -> send rows -> ncclSend/Recv into the
+    ghost rows, ncclAllReduce(max) of [smax, status], separate finalize kernel) run
+    as a 1-rank self exchange: same bits as the local path and the oracle."""
+    cfg = O.Config(nx=150, ny=96, system=O.EULER, param=(G,), bc_y=bc_y)
+    W0 = inputs.euler_random(150, 96, seed=12)
+    ref = O.run(cfg, W0, 40, O.ADAPTIVE, 0.45)
+    W, log = gpu_run(cfg, W0, 40, O.ADAPTIVE, 0.45, flags=fv2d.FLAG_NCCL_LOOPBACK,
+                     nccl_id=fv2d.nccl_unique_id())
+    assert np.array_equal(log, ref.dt_log) and np.array_equal(W, ref.W)
+
+
+def test_nccl_loopback_cfl_error_and_spray():
+    n = 64
+    cfg = O.Config(nx=n, ny=n, system=O.EULER, param=(G,))
+    W0 = inputs.euler_bell(n, n)
+    s0, arg0 = O.smax(cfg, W0)
+    with solver_for(cfg, flags=fv2d.FLAG_NCCL_LOOPBACK, nccl_id=fv2d.nccl_unique_id()) as s:
+        s.set_state(W0)
+        s.step((1 / n) / s0 * 1.0000001, 3)
+        with pytest.raises(fv2d.FV2DError) as e:
+            s.synchronize()
+        assert e.value.code == fv2d.E_CFL and e.value.step == 0
+        assert np.array_equal(s.get_state(raise_on_error=False), W0)
+    scfg, S0, dt = spray_case(48)
+    ref = O.run(scfg, S0, 5, O.FIXED, dt)
+    W, _ = gpu_run(scfg, S0, 5, O.FIXED, dt, flags=fv2d.FLAG_NCCL_LOOPBACK,
+                   nccl_id=fv2d.nccl_unique_id())
+    assert relerr(W, ref.W) <= 1e-10
