@@ -134,8 +134,12 @@ struct fv2d_ctx {
   long long dt_log_cap = 0;
   unsigned long long* newton = nullptr;
   double* trig = nullptr;  // sx[nx] cx[nx] sy[ny] cy[ny]
+  double* lam_cache = nullptr;  // spray: Newton warm start, nslabs x H x 4 x pitch
+  bool lam_valid = false;
   ncclComm_t comm = nullptr;
   bool use_nccl = false;  // nranks > 1, or FV2D_FLAG_NCCL_LOOPBACK (self exchange on 1 rank)
+  cudaStream_t comm_stream = nullptr;  // NCCL halo exchange overlapped with the interior pass
+  cudaEvent_t ev_bnd = nullptr, ev_int = nullptr, ev_fin = nullptr;
   // host state
   bool has_state = false;
   bool dt_valid = false;
@@ -222,6 +226,17 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   }
 }
 
+// Row ranges of a marching-kernel launch (see StepArgs).
+void set_ranges(StepArgs& a, int lo0, int hi0, int rps0, int lo1, int hi1, int rps1) {
+  a.row_lo[0] = lo0; a.row_hi[0] = hi0; a.rps[0] = rps0;
+  a.row_lo[1] = lo1; a.row_hi[1] = hi1; a.rps[1] = rps1;
+  a.nstrips0 = hi0 > lo0 ? (hi0 - lo0 + rps0 - 1) / rps0 : 0;
+  a.nranges = hi1 > lo1 ? 2 : 1;
+}
+int total_strips(const StepArgs& a) {
+  return a.nstrips0 + (a.row_hi[1] > a.row_lo[1] ? (a.row_hi[1] - a.row_lo[1] + a.rps[1] - 1) / a.rps[1] : 0);
+}
+
 // Arguments of a pass reading parity p (and writing parity 1-p).
 StepArgs make_args(const fv2d_ctx* ctx, int p) {
   StepArgs a;
@@ -239,7 +254,7 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.nx = ctx->nx;
   a.pitch = ctx->pitch;
   a.rs = ctx->rs;
-  a.rows_per_strip = ctx->rps;
+  set_ranges(a, 0, ctx->H, ctx->rps, 0, 0, 1);
   a.bcx = ctx->cfg.bc_x;
   for (int v = 0; v < kMaxVar; ++v) a.dirx[v] = ctx->cfg.dirichlet[v];
   a.dx = ctx->dx;
@@ -266,6 +281,8 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
     a.cy_tab = ctx->trig + 2 * ctx->nx + ctx->cfg.ny;
   }
   a.newton_iters = ctx->newton;
+  a.lam_cache = ctx->lam_cache;
+  a.lam_valid = ctx->lam_valid ? 1 : 0;
   return a;
 }
 
@@ -291,21 +308,21 @@ struct LaunchStep {
       // spray (nVar 6) uses the one-cell kernel: its fused source needs the registers
       if constexpr (Sys::NV == 6) {
         const int cols = 30 * kWarps;
-        dim3 grid((ctx->nx + cols - 1) / cols, (ctx->H + ctx->rps - 1) / ctx->rps, ctx->nslabs);
+        dim3 grid((ctx->nx + cols - 1) / cols, total_strips(a), ctx->nslabs);
         if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
       } else if (ctx->cfg.flags & FV2D_FLAG_ONE_CELL) {
         const int cols = 30 * kWarps;
-        dim3 grid((ctx->nx + cols - 1) / cols, (ctx->H + ctx->rps - 1) / ctx->rps, ctx->nslabs);
+        dim3 grid((ctx->nx + cols - 1) / cols, total_strips(a), ctx->nslabs);
         if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
       } else {
         const int warps = (ctx->nx + 1 + 61) / 62;
-        dim3 grid((warps + kWarps - 1) / kWarps, (ctx->H + ctx->rps - 1) / ctx->rps, ctx->nslabs);
+        dim3 grid((warps + kWarps - 1) / kWarps, total_strips(a), ctx->nslabs);
         if (xper && !a.adaptive) fv_step_pair_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (xper && a.adaptive) fv_step_pair_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
         if (!xper && !a.adaptive) fv_step_pair_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
@@ -336,24 +353,26 @@ struct LaunchArgmax {
 int cur_parity(const fv2d_ctx* ctx) { return (int)(ctx->steps & 1); }
 
 // NCCL halo exchange into ghost buffers of parity q, from send_s/send_n.
-fv2d_status exchange(fv2d_ctx* ctx, int q) {
+fv2d_status exchange(fv2d_ctx* ctx, int q, cudaStream_t stream = nullptr) {
   if (!ctx->use_nccl) return FV2D_OK;
+  if (!stream) stream = ctx->stream;
   const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
   const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
   const bool has_s = r > 0 || per, has_n = r < P - 1 || per;
   const size_t cnt = (size_t)ctx->rs;  // one whole cell row: nv variable rows
   CKN(g_nccl.GroupStart());
-  if (has_s) CKN(g_nccl.Send(ctx->send_s, cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, ctx->stream));
-  if (has_n) CKN(g_nccl.Recv(ghost_n(ctx, 0, q), cnt, ncclFloat64, (r + 1) % P, ctx->comm, ctx->stream));
-  if (has_n) CKN(g_nccl.Send(ctx->send_n, cnt, ncclFloat64, (r + 1) % P, ctx->comm, ctx->stream));
-  if (has_s) CKN(g_nccl.Recv(ghost_s(ctx, 0, q), cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, ctx->stream));
+  if (has_s) CKN(g_nccl.Send(ctx->send_s, cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, stream));
+  if (has_n) CKN(g_nccl.Recv(ghost_n(ctx, 0, q), cnt, ncclFloat64, (r + 1) % P, ctx->comm, stream));
+  if (has_n) CKN(g_nccl.Send(ctx->send_n, cnt, ncclFloat64, (r + 1) % P, ctx->comm, stream));
+  if (has_s) CKN(g_nccl.Recv(ghost_s(ctx, 0, q), cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, stream));
   CKN(g_nccl.GroupEnd());
   return FV2D_OK;
 }
 
 // max-all-reduce of [smax bits, pending status] into dscal[4..5].
-fv2d_status allreduce_scalars(fv2d_ctx* ctx) {
-  CKN(g_nccl.AllReduce(ctx->dscal + 0, ctx->dscal + 4, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+fv2d_status allreduce_scalars(fv2d_ctx* ctx, cudaStream_t stream = nullptr) {
+  CKN(g_nccl.AllReduce(ctx->dscal + 0, ctx->dscal + 4, 2, ncclUint64, ncclMax, ctx->comm,
+                       stream ? stream : ctx->stream));
   return FV2D_OK;
 }
 
@@ -510,8 +529,13 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   if (ctx->dt_log) cudaFree(ctx->dt_log);
   if (ctx->newton) cudaFree(ctx->newton);
   if (ctx->trig) cudaFree(ctx->trig);
+  if (ctx->lam_cache) cudaFree(ctx->lam_cache);
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
+  if (ctx->ev_int) cudaEventDestroy(ctx->ev_int);
+  if (ctx->ev_fin) cudaEventDestroy(ctx->ev_fin);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   delete ctx;
   return FV2D_OK;
 }
@@ -582,6 +606,10 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
       CKC(cudaMemset(ctx->buf[s][p], 0, state_bytes));
     }
   if (use_nccl) {
+    CKC(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_bnd, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_int, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_fin, cudaEventDisableTiming));
     CKC(cudaMalloc(&ctx->send_s, row_bytes));
     CKC(cudaMalloc(&ctx->send_n, row_bytes));
     CKC(cudaMemset(ctx->send_s, 0, row_bytes));
@@ -598,6 +626,7 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   CKC(cudaMemset(ctx->newton, 0, sizeof(unsigned long long)));
   if (c.system == FV2D_SPRAY) {
     CKC(cudaMalloc(&ctx->trig, (size_t)(2 * c.nx + 2 * c.ny) * sizeof(double)));
+    CKC(cudaMalloc(&ctx->lam_cache, (size_t)ctx->nslabs * H * 4 * ctx->pitch * sizeof(double)));
     trig_table_kernel<<<(c.nx + 255) / 256, 256>>>(ctx->trig, ctx->trig + c.nx, c.nx, c.x0, ctx->dx);
     trig_table_kernel<<<(c.ny + 255) / 256, 256>>>(ctx->trig + 2 * c.nx, ctx->trig + 2 * c.nx + c.ny, c.ny, c.y0,
                                                     ctx->dy);
@@ -655,6 +684,7 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->has_state = true;
   ctx->dt_valid = false;
+  ctx->lam_valid = false;
   ctx->err.clear();
   ctx->err_step = ctx->err_cell = -1;
   return FV2D_OK;
@@ -840,6 +870,34 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
       if (st) return st;
       CK(cudaEventRecord(e0, ctx->stream));
     }
+    // NCCL path for transport-only systems: boundary strips first, halo
+    // exchange on the comm stream overlapped with the interior strips.
+    const int hb = 8;
+    const bool overlap = ctx->use_nccl && !split && !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H > 4 * hb;
+    if (overlap) {
+      StepArgs ab = at, ai = at;
+      set_ranges(ab, 0, hb, hb, ctx->H - hb, ctx->H, hb);
+      set_ranges(ai, hb, ctx->H - hb, ctx->rps, 0, 0, 1);
+      dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, ab);
+      CKL();
+      CK(cudaEventRecord(ctx->ev_bnd, ctx->stream));
+      CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_bnd, 0));
+      st = exchange(ctx, 1 - p, ctx->comm_stream);
+      if (st) return st;
+      dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, ai);
+      CKL();
+      if (ctx->profiling) CK(cudaEventRecord(e1, ctx->stream));
+      CK(cudaEventRecord(ctx->ev_int, ctx->stream));
+      CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_int, 0));
+      st = allreduce_scalars(ctx, ctx->comm_stream);
+      if (st) return st;
+      finalize_kernel<<<1, 32, 0, ctx->comm_stream>>>(a, ctx->dscal + 4);
+      CKL();
+      CK(cudaEventRecord(ctx->ev_fin, ctx->comm_stream));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_fin, 0));
+      ctx->steps += 1;
+      continue;
+    }
     dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, at);
     CKL();
     if (ctx->profiling) CK(cudaEventRecord(e1, ctx->stream));
@@ -849,6 +907,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
       dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
       spray_source_dt_kernel_launch(ctx, a, grid);
       CKL();
+      ctx->lam_valid = true;
     }
     if (ctx->use_nccl) {
       st = exchange(ctx, 1 - p);
@@ -908,6 +967,7 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
   spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt, 0);
   CKL();
+  ctx->lam_valid = true;
   fv2d_status st = exchange(ctx, p);
   if (st) return st;
   promote_pending_kernel<<<1, 32, 0, ctx->stream>>>(ctx->dscal + 1, ctx->dscal + 2);
