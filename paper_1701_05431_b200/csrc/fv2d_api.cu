@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -118,6 +119,7 @@ struct fv2d_ctx {
   fv2d_config cfg{};
   cudaStream_t stream = nullptr;
   int nv = 0, nx = 0, H = 0, pitch = 0, nslabs = 1, G = 1, rps = 64;
+  int ring_depth = 4;  // rows in the pair kernel's per-warp prefetch ring
   long long rs = 0;  // row stride (nv * pitch); a buffer holds rows -1..H
   double dx = 0, dy = 0, hmin = 0;
   // per local slab: two ping-pong buffers of (H+2) rows (ghost rows -1 and H inside)
@@ -296,6 +298,26 @@ void dispatch(int system, Args&&... args) {
   }
 }
 
+template <class Sys, int D, bool XPER, bool ADAPT>
+void launch_pair_1(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
+  auto k = fv_step_pair_kernel<Sys, XPER, ADAPT, kWarps, D>;
+  const int smem = kWarps * D * Sys::NV * 64 * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k<<<grid, kWarps * 32, smem, ctx->stream>>>(a);
+}
+
+template <class Sys, int D>
+void launch_pair(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid, bool xper) {
+  if (xper && !a.adaptive) launch_pair_1<Sys, D, true, false>(ctx, a, grid);
+  if (xper && a.adaptive) launch_pair_1<Sys, D, true, true>(ctx, a, grid);
+  if (!xper && !a.adaptive) launch_pair_1<Sys, D, false, false>(ctx, a, grid);
+  if (!xper && a.adaptive) launch_pair_1<Sys, D, false, true>(ctx, a, grid);
+}
+
 template <class Sys>
 struct LaunchStep {
   static void run(const fv2d_ctx* ctx, const StepArgs& a) {
@@ -323,10 +345,11 @@ struct LaunchStep {
       } else {
         const int warps = (ctx->nx + 1 + 61) / 62;
         dim3 grid((warps + kWarps - 1) / kWarps, total_strips(a), ctx->nslabs);
-        if (xper && !a.adaptive) fv_step_pair_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (xper && a.adaptive) fv_step_pair_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (!xper && !a.adaptive) fv_step_pair_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (!xper && a.adaptive) fv_step_pair_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        switch (ctx->ring_depth) {
+          case 6: launch_pair<Sys, 6>(ctx, a, grid, xper); break;
+          case 8: launch_pair<Sys, 8>(ctx, a, grid, xper); break;
+          default: launch_pair<Sys, 4>(ctx, a, grid, xper); break;
+        }
       }
     }
   }
@@ -568,6 +591,7 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   ctx->nx = c.nx;
   ctx->H = (int)H;
   ctx->pitch = (c.nx + 31) / 32 * 32;
+  if (const char* e = getenv("FV2D_RING_DEPTH")) ctx->ring_depth = atoi(e);  // tuning knob
   ctx->rs = (long long)ctx->pitch * nv;
   {
     // strip height of the marching kernel: ~2 waves of 3 CTAs per SM for large
