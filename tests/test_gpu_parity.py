@@ -327,3 +327,17 @@ def test_nccl_loopback_cfl_error_and_spray():
     W, _ = gpu_run(scfg, S0, 5, O.FIXED, dt, flags=fv2d.FLAG_NCCL_LOOPBACK,
                    nccl_id=fv2d.nccl_unique_id())
     assert relerr(W, ref.W) <= 1e-10
+
+
+def test_gpu_first_order_convergence_bell_and_vortex():
+    """fig:Convergence on the GPU path: L1 slopes of rho vs the
+    analytic solutions approach 1 (the paper reports ~0.95) for the bell (R22)
+    and the isentropic vortex (R21), T = 0.1, 128^2 .. 1024^2."""
+    import sys
+    sys.path.insert(0, __import__("os").path.join(__import__("os").path.dirname(__file__), "..", "tools"))
+    from convergence import errors
+    for case in ("bell", "vortex"):
+        errs = [errors(case, n, 0.1)["L1"] for n in (128, 256, 512, 1024)]
+        slopes = [math.log2(errs[k] / errs[k + 1]) for k in range(3)]
+        assert all(0.85 <= s <= 1.05 for s in slopes), (case, slopes)
+        assert slopes[-1] >= 0.9, (case, slopes)
