@@ -77,6 +77,9 @@ typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
 #define FV2D_FLAG_FUSE_SOURCE 0x10u /* spray: apply the source in the transport pass's
                                         epilogue (one pass, 96 B/cell less traffic; lower
                                         occupancy for the FP64-bound Newton, slower on B200) */
+#define FV2D_FLAG_GRAPH 0x20u      /* replay each step from a CUDA graph captured once per
+                                        ping-pong parity (re-captured when dt/mode change);
+                                        single-process contexts only */
 #define FV2D_FLAG_NCCL_LOOPBACK 0x8u /* take the NCCL halo/all-reduce path even with
                                         nranks == 1 (self send/recv; needs an id from
                                         fv2d_nccl_unique_id); exercises the multi-GPU
@@ -95,7 +98,11 @@ typedef struct {
                               ghost rows are exchanged exactly like the ranks' */
   int32_t device;          /* CUDA device ordinal */
   uint32_t flags;          /* FV2D_FLAG_* */
-  int32_t reserved[7];     /* must be 0 */
+  int32_t tiles_x, tiles_y; /* 0/1: one launch per step.  > 1: each step is launched as
+                              tiles_x x tiles_y separate sub-launches over the slab (the
+                              paper's NPartX x NPartY task decomposition, P:215-220;
+                              granularity study P:741-754).  Same bits. */
+  int32_t reserved[5];     /* must be 0 */
 } fv2d_config;
 
 typedef struct fv2d_ctx fv2d_ctx;

@@ -120,6 +120,16 @@ struct fv2d_ctx {
   cudaStream_t stream = nullptr;
   int nv = 0, nx = 0, H = 0, pitch = 0, nslabs = 1, G = 1, rps = 64;
   int ring_depth = 4;  // rows in the pair kernel's per-warp prefetch ring
+  int tiles_x = 1, tiles_y = 1;  // launch decomposition of a step (granularity study)
+  cudaStream_t launch_stream = nullptr;  // stream kernels are launched on (capture stream while capturing)
+  // CUDA graph of one step per parity (FV2D_FLAG_GRAPH)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  bool graph_ready = false;
+  int graph_adaptive = -1;
+  double graph_dt = 0.0, graph_cfl = 0.0;
+  bool graph_lam_valid = false;
+  const double* graph_dt_log = nullptr;
   long long rs = 0;  // row stride (nv * pitch); a buffer holds rows -1..H
   double dx = 0, dy = 0, hmin = 0;
   // per local slab: two ping-pong buffers of (H+2) rows (ghost rows -1 and H inside)
@@ -228,6 +238,16 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   }
 }
 
+// Strip height of a marching-kernel launch over ncols x nrows cells: ~2 waves
+// of 3 CTAs per SM for large launches (128 rows: 1.6% halo-row overhead), down
+// to 4 rows for small ones, where the serial march of a strip (latency), not
+// bandwidth, bounds the launch.
+int pick_rps(int ncols, int nrows) {
+  const long long colblocks = ((ncols + 62) / 62 + kWarps - 1) / kWarps;
+  const long long rps = colblocks * nrows / (148 * 6);
+  return (int)std::max<long long>(4, std::min<long long>(128, rps));
+}
+
 // Row ranges of a marching-kernel launch (see StepArgs).
 void set_ranges(StepArgs& a, int lo0, int hi0, int rps0, int lo1, int hi1, int rps1) {
   a.row_lo[0] = lo0; a.row_hi[0] = hi0; a.rps[0] = rps0;
@@ -283,6 +303,9 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
     a.cy_tab = ctx->trig + 2 * ctx->nx + ctx->cfg.ny;
   }
   a.newton_iters = ctx->newton;
+  a.step_dev = reinterpret_cast<long long*>(ctx->dscal + 6);
+  a.col_lo = 0;
+  a.col_hi = ctx->nx;
   a.lam_cache = ctx->lam_cache;
   a.lam_valid = ctx->lam_valid ? 1 : 0;
   return a;
@@ -307,7 +330,7 @@ void launch_pair_1(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  k<<<grid, kWarps * 32, smem, ctx->stream>>>(a);
+  k<<<grid, kWarps * 32, smem, ctx->launch_stream>>>(a);
 }
 
 template <class Sys, int D>
@@ -323,27 +346,27 @@ struct LaunchStep {
   static void run(const fv2d_ctx* ctx, const StepArgs& a) {
     if (ctx->cfg.flags & FV2D_FLAG_NAIVE) {
       dim3 grid((ctx->nx + 31) / 32, (ctx->H + 7) / 8, ctx->nslabs);
-      fv_step_naive_kernel<Sys><<<grid, 256, 0, ctx->stream>>>(a);
+      fv_step_naive_kernel<Sys><<<grid, 256, 0, ctx->launch_stream>>>(a);
     } else {
       constexpr int D = 4;
       const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC;
       // spray (nVar 6) uses the one-cell kernel: its fused source needs the registers
       if constexpr (Sys::NV == 6) {
         const int cols = 30 * kWarps;
-        dim3 grid((ctx->nx + cols - 1) / cols, total_strips(a), ctx->nslabs);
-        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        dim3 grid((a.col_hi - a.col_lo + cols - 1) / cols, total_strips(a), ctx->nslabs);
+        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
+        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
+        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
+        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
       } else if (ctx->cfg.flags & FV2D_FLAG_ONE_CELL) {
         const int cols = 30 * kWarps;
-        dim3 grid((ctx->nx + cols - 1) / cols, total_strips(a), ctx->nslabs);
-        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
-        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->stream>>>(a);
+        dim3 grid((a.col_hi - a.col_lo + cols - 1) / cols, total_strips(a), ctx->nslabs);
+        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
+        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
+        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
+        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
       } else {
-        const int warps = (ctx->nx + 1 + 61) / 62;
+        const int warps = (a.col_hi - a.col_lo + 1 + 61) / 62;
         dim3 grid((warps + kWarps - 1) / kWarps, total_strips(a), ctx->nslabs);
         switch (ctx->ring_depth) {
           case 6: launch_pair<Sys, 6>(ctx, a, grid, xper); break;
@@ -559,6 +582,9 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   if (ctx->ev_int) cudaEventDestroy(ctx->ev_int);
   if (ctx->ev_fin) cudaEventDestroy(ctx->ev_fin);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  for (int p = 0; p < 2; ++p)
+    if (ctx->graph[p]) cudaGraphExecDestroy(ctx->graph[p]);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
   return FV2D_OK;
 }
@@ -576,10 +602,12 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   if (c.system == FV2D_ADVECTION && (c.bc_x == FV2D_BC_WALL || c.bc_y == FV2D_BC_WALL)) return FV2D_E_ARG;
   if (c.system == FV2D_EULER && !(c.param[0] > 1.0)) return FV2D_E_ARG;
   if (c.system == FV2D_SPRAY && !(c.param[1] > 0.0)) return FV2D_E_ARG;
-  for (int k = 0; k < 7; ++k)
+  for (int k = 0; k < 5; ++k)
     if (c.reserved[k] != 0) return FV2D_E_ARG;
+  if (c.tiles_x < 0 || c.tiles_y < 0 || c.tiles_x > 256 || c.tiles_y > 256) return FV2D_E_ARG;
   const long long H = c.ny / (c.nranks * c.nslabs);
   if (H < 1) return FV2D_E_ARG;
+  if (std::max(1, c.tiles_y) > H || 2 * std::max(1, c.tiles_x) > c.nx) return FV2D_E_ARG;
   const bool use_nccl = c.nranks > 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK);
   if (use_nccl && (!nccl_id || !load_nccl())) return FV2D_E_NCCL;
 
@@ -587,20 +615,16 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   ctx->cfg = c;
   ctx->use_nccl = use_nccl;
   ctx->stream = (cudaStream_t)cuda_stream;
+  ctx->launch_stream = ctx->stream;
+  ctx->tiles_x = std::max(1, c.tiles_x);
+  ctx->tiles_y = std::max(1, c.tiles_y);
   ctx->nv = nv;
   ctx->nx = c.nx;
   ctx->H = (int)H;
   ctx->pitch = (c.nx + 31) / 32 * 32;
   if (const char* e = getenv("FV2D_RING_DEPTH")) ctx->ring_depth = atoi(e);  // tuning knob
   ctx->rs = (long long)ctx->pitch * nv;
-  {
-    // strip height of the marching kernel: ~2 waves of 3 CTAs per SM for large
-    // grids (128 rows: 1.6% halo-row overhead), down to 4 rows for small grids
-    // where latency, not bandwidth, bounds the step
-    const long long colblocks = ((c.nx + 62) / 62 + kWarps - 1) / kWarps;
-    long long rps = colblocks * H / (148 * 6);
-    ctx->rps = (int)std::max<long long>(4, std::min<long long>(128, rps));
-  }
+  ctx->rps = pick_rps(c.nx, (int)H);
   ctx->nslabs = c.nslabs;
   ctx->G = c.nranks * c.nslabs;
   ctx->dx = (c.x1 - c.x0) / c.nx;
@@ -864,86 +888,156 @@ static fv2d_status prof_events(fv2d_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1) 
 
 // The split source pass of a step: dt is the fixed dt or, in adaptive mode,
 // the device scalar (read inside the kernel so the launch stays asynchronous).
-static void spray_source_dt_kernel_launch(fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
+static void spray_source_dt_kernel_launch(fv2d_ctx* ctx, const StepArgs& a, dim3 grid, int p) {
   StepArgs b = a;
-  for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, 1 - (int)(ctx->steps & 1), 0);
-  spray_source_step_kernel<<<grid, 128, 0, ctx->stream>>>(b);
+  for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, 1 - p, 0);
+  spray_source_step_kernel<<<grid, 128, 0, ctx->launch_stream>>>(b);
+}
+
+// The launches of one time step reading parity p, on ctx->launch_stream (the
+// caller's stream, or the capture stream while recording a CUDA graph).
+static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, double cfl, cudaEvent_t e1) {
+  fv2d_status st = FV2D_OK;
+  const bool split = ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE);
+  const bool tiled = ctx->tiles_x * ctx->tiles_y > 1 && !(ctx->cfg.flags & FV2D_FLAG_NAIVE);
+  StepArgs a = make_args(ctx, p);
+  a.adaptive = adaptive;
+  a.dt = dt;
+  a.cfl = cfl;
+  a.step = ctx->steps;
+  if (ctx->use_nccl || tiled) a.fused_finalize = 0;
+  StepArgs at = a;  // transport pass
+  if (split) {
+    at.fuse_source = 0;
+    at.fused_finalize = 0;  // the source pass ends the step
+    at.no_smax = 1;         // adaptive: smax of the post-source state comes from the source pass
+  }
+  cudaStream_t ls = ctx->launch_stream;
+  // NCCL path for transport-only systems: boundary strips first, halo
+  // exchange on the comm stream overlapped with the interior strips.
+  const int hb = 8;
+  const bool overlap =
+      ctx->use_nccl && !split && !tiled && !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H > 4 * hb;
+  if (overlap) {
+    StepArgs ab = at, ai = at;
+    set_ranges(ab, 0, hb, hb, ctx->H - hb, ctx->H, hb);
+    set_ranges(ai, hb, ctx->H - hb, ctx->rps, 0, 0, 1);
+    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, ab);
+    CKL();
+    CK(cudaEventRecord(ctx->ev_bnd, ls));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_bnd, 0));
+    st = exchange(ctx, 1 - p, ctx->comm_stream);
+    if (st) return st;
+    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, ai);
+    CKL();
+    if (e1) CK(cudaEventRecord(e1, ls));
+    CK(cudaEventRecord(ctx->ev_int, ls));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_int, 0));
+    st = allreduce_scalars(ctx, ctx->comm_stream);
+    if (st) return st;
+    finalize_kernel<<<1, 32, 0, ctx->comm_stream>>>(a, ctx->dscal + 4);
+    CKL();
+    CK(cudaEventRecord(ctx->ev_fin, ctx->comm_stream));
+    CK(cudaStreamWaitEvent(ls, ctx->ev_fin, 0));
+    return FV2D_OK;
+  }
+  if (tiled) {
+    // the domain as tiles_x x tiles_y separate launches (the paper's NPartX x
+    // NPartY tasks, P:215-220 / P:741-754); column cuts on even columns
+    for (int ty = 0; ty < ctx->tiles_y; ++ty)
+      for (int tx = 0; tx < ctx->tiles_x; ++tx) {
+        StepArgs t = at;
+        const int r_lo = (int)((long long)ty * ctx->H / ctx->tiles_y);
+        const int r_hi = (int)((long long)(ty + 1) * ctx->H / ctx->tiles_y);
+        t.col_lo = (int)((long long)tx * ctx->nx / ctx->tiles_x) & ~1;
+        t.col_hi = tx + 1 == ctx->tiles_x ? ctx->nx : (int)((long long)(tx + 1) * ctx->nx / ctx->tiles_x) & ~1;
+        set_ranges(t, r_lo, r_hi, pick_rps(t.col_hi - t.col_lo, r_hi - r_lo), 0, 0, 1);
+        dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, t);
+        CKL();
+      }
+  } else {
+    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, at);
+    CKL();
+  }
+  if (e1) CK(cudaEventRecord(e1, ls));
+  if (split) {
+    // in place on the transport output; dt: the fixed dt, or read from the
+    // device in adaptive mode (the finalize writes dt_{n+1} only after this pass)
+    dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
+    StepArgs b = a;
+    if (tiled) b.fused_finalize = 0;
+    spray_source_dt_kernel_launch(ctx, b, grid, p);
+    CKL();
+  }
+  if (ctx->use_nccl) {
+    st = exchange(ctx, 1 - p, ls);
+    if (st) return st;
+    st = allreduce_scalars(ctx, ls);
+    if (st) return st;
+    finalize_kernel<<<1, 32, 0, ls>>>(a, ctx->dscal + 4);
+    CKL();
+  } else if (!a.fused_finalize) {
+    finalize_kernel<<<1, 32, 0, ls>>>(a, nullptr);
+    CKL();
+  }
+  return FV2D_OK;
+}
+
+// Record one step per parity into CUDA graphs (FV2D_FLAG_GRAPH).
+static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double cfl) {
+  if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  for (int p = 0; p < 2; ++p) {
+    if (ctx->graph[p]) {
+      CK(cudaGraphExecDestroy(ctx->graph[p]));
+      ctx->graph[p] = nullptr;
+    }
+    cudaGraph_t g;
+    ctx->launch_stream = ctx->cap_stream;
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    fv2d_status st = issue_step(ctx, p, adaptive, dt, cfl, nullptr);
+    cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
+    ctx->launch_stream = ctx->stream;
+    if (st) return st;
+    if (ce != cudaSuccess) return set_err(ctx, FV2D_E_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+    CK(cudaGraphInstantiate(&ctx->graph[p], g, 0));
+    CK(cudaGraphDestroy(g));
+  }
+  ctx->graph_ready = true;
+  ctx->graph_adaptive = adaptive;
+  ctx->graph_dt = dt;
+  ctx->graph_cfl = cfl;
+  ctx->graph_lam_valid = ctx->lam_valid;
+  ctx->graph_dt_log = ctx->dt_log;
+  return FV2D_OK;
 }
 
 static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double cfl, int32_t nsteps) {
   fv2d_status st = ensure_dt_log(ctx, ctx->steps + nsteps);
   if (st) return st;
   const bool split = ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE);
+  const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl;
   for (int32_t k = 0; k < nsteps; ++k) {
     const int p = cur_parity(ctx);
-    StepArgs a = make_args(ctx, p);
-    a.adaptive = adaptive;
-    a.dt = dt;
-    a.cfl = cfl;
-    a.step = ctx->steps;
-    if (ctx->use_nccl) a.fused_finalize = 0;
-    StepArgs at = a;  // transport pass
-    if (split) {
-      at.fuse_source = 0;
-      at.fused_finalize = 0;  // the source pass ends the step
-      at.no_smax = 1;         // adaptive: smax of the post-source state comes from the source pass
-    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->profiling) {
       st = prof_events(ctx, &e0, &e1);
       if (st) return st;
       CK(cudaEventRecord(e0, ctx->stream));
     }
-    // NCCL path for transport-only systems: boundary strips first, halo
-    // exchange on the comm stream overlapped with the interior strips.
-    const int hb = 8;
-    const bool overlap = ctx->use_nccl && !split && !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H > 4 * hb;
-    if (overlap) {
-      StepArgs ab = at, ai = at;
-      set_ranges(ab, 0, hb, hb, ctx->H - hb, ctx->H, hb);
-      set_ranges(ai, hb, ctx->H - hb, ctx->rps, 0, 0, 1);
-      dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, ab);
-      CKL();
-      CK(cudaEventRecord(ctx->ev_bnd, ctx->stream));
-      CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_bnd, 0));
-      st = exchange(ctx, 1 - p, ctx->comm_stream);
+    if (use_graph) {
+      if (!ctx->graph_ready || ctx->graph_adaptive != adaptive || ctx->graph_dt != dt || ctx->graph_cfl != cfl ||
+          ctx->graph_lam_valid != ctx->lam_valid || ctx->graph_dt_log != ctx->dt_log) {
+        st = capture_graphs(ctx, adaptive, dt, cfl);
+        if (st) return st;
+      }
+      CK(cudaGraphLaunch(ctx->graph[p], ctx->stream));
+      ctx->launches += 1;
+      if (e1) CK(cudaEventRecord(e1, ctx->stream));
+    } else {
+      st = issue_step(ctx, p, adaptive, dt, cfl, e1);
       if (st) return st;
-      dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, ai);
-      CKL();
-      if (ctx->profiling) CK(cudaEventRecord(e1, ctx->stream));
-      CK(cudaEventRecord(ctx->ev_int, ctx->stream));
-      CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_int, 0));
-      st = allreduce_scalars(ctx, ctx->comm_stream);
-      if (st) return st;
-      finalize_kernel<<<1, 32, 0, ctx->comm_stream>>>(a, ctx->dscal + 4);
-      CKL();
-      CK(cudaEventRecord(ctx->ev_fin, ctx->comm_stream));
-      CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_fin, 0));
-      ctx->steps += 1;
-      continue;
     }
-    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, at);
-    CKL();
-    if (ctx->profiling) CK(cudaEventRecord(e1, ctx->stream));
-    if (split) {
-      // in place on the transport output; dt: the fixed dt, or read from the
-      // device in adaptive mode (the finalize writes dt_{n+1} only after this pass)
-      dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
-      spray_source_dt_kernel_launch(ctx, a, grid);
-      CKL();
-      ctx->lam_valid = true;
-    }
-    if (ctx->use_nccl) {
-      st = exchange(ctx, 1 - p);
-      if (st) return st;
-      st = allreduce_scalars(ctx);
-      if (st) return st;
-      finalize_kernel<<<1, 32, 0, ctx->stream>>>(a, ctx->dscal + 4);
-      CKL();
-    } else if (!a.fused_finalize) {
-      finalize_kernel<<<1, 32, 0, ctx->stream>>>(a, nullptr);
-      CKL();
-    }
+    if (split) ctx->lam_valid = true;
     ctx->steps += 1;
   }
   return FV2D_OK;

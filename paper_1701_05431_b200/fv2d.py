@@ -18,7 +18,8 @@ OK, E_ARG, E_CFL, E_NONFINITE, E_RECON, E_CUDA, E_NCCL, E_STATE = range(8)
 ADVECTION, EULER, SPRAY = 0, 1, 2
 BC_PERIODIC, BC_DIRICHLET, BC_WALL = 0, 1, 2
 AOS, SOA = 0, 1
-FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL, FLAG_NCCL_LOOPBACK, FLAG_FUSE_SOURCE = 0x1, 0x2, 0x4, 0x8, 0x10
+FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL, FLAG_NCCL_LOOPBACK, FLAG_FUSE_SOURCE, FLAG_GRAPH = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
 NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
 _NAMES = {OK: "OK", E_ARG: "E_ARG", E_CFL: "E_CFL", E_NONFINITE: "E_NONFINITE", E_RECON: "E_RECON",
           E_CUDA: "E_CUDA", E_NCCL: "E_NCCL", E_STATE: "E_STATE"}
@@ -30,7 +31,8 @@ class Config(C.Structure):
                 ("x0", C.c_double), ("x1", C.c_double), ("y0", C.c_double), ("y1", C.c_double),
                 ("param", C.c_double * 8), ("dirichlet", C.c_double * 6),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("nslabs", C.c_int32), ("device", C.c_int32),
-                ("flags", C.c_uint32), ("reserved", C.c_int32 * 7)]
+                ("flags", C.c_uint32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
+                ("reserved", C.c_int32 * 5)]
 
 
 class Stats(C.Structure):
@@ -119,7 +121,7 @@ class Solver:
 
     def __init__(self, nx, ny, system=EULER, *, x0=0.0, x1=1.0, y0=0.0, y1=1.0, param=None,
                  bc_x=BC_PERIODIC, bc_y=BC_PERIODIC, dirichlet=(), rank=0, nranks=1, nslabs=1, device=0,
-                 flags=0, nccl_id: bytes | None = None, stream: int | None = None):
+                 flags=0, tiles=(1, 1), nccl_id: bytes | None = None, stream: int | None = None):
         L = lib()
         cfg = Config()
         rc = L.fv2d_config_default(C.byref(cfg), nx, ny, system)
@@ -135,6 +137,7 @@ class Solver:
             cfg.dirichlet[k] = v
         cfg.bc_x, cfg.bc_y = bc_x, bc_y
         cfg.rank, cfg.nranks, cfg.nslabs, cfg.device, cfg.flags = rank, nranks, nslabs, device, flags
+        cfg.tiles_x, cfg.tiles_y = tiles
         self.cfg = cfg
         self.nx, self.ny, self.nv, self.system = nx, ny, NVAR[system], system
         self.ny_local = ny // nranks

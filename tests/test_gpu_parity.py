@@ -341,3 +341,59 @@ def test_gpu_first_order_convergence_bell_and_vortex():
         slopes = [math.log2(errs[k] / errs[k + 1]) for k in range(3)]
         assert all(0.85 <= s <= 1.05 for s in slopes), (case, slopes)
         assert slopes[-1] >= 0.9, (case, slopes)
+
+
+@pytest.mark.parametrize("tiles", [(3, 5), (8, 8), (1, 7), (16, 2)])
+def test_tiled_launches_same_bits(tiles):
+    """The step as tiles_x x tiles_y sub-launches (the paper's NPartX x NPartY tasks,
+    P:215-220) gives the same bits, periodic and wall."""
+    for bc in (O.BC_PERIODIC, O.BC_WALL):
+        cfg = O.Config(nx=300, ny=200, system=O.EULER, param=(G,), x1=1.5, bc_x=bc, bc_y=bc)
+        W0 = inputs.euler_random(300, 200, seed=31)
+        ref = O.run(cfg, W0, 12, O.ADAPTIVE, 0.45)
+        W, log = gpu_run(cfg, W0, 12, O.ADAPTIVE, 0.45, tiles=tiles)
+        assert np.array_equal(log, ref.dt_log) and np.array_equal(W, ref.W)
+
+
+@pytest.mark.parametrize("flags,tiles", [(fv2d.FLAG_GRAPH, (1, 1)), (fv2d.FLAG_GRAPH, (4, 4)),
+                                         (fv2d.FLAG_GRAPH | fv2d.FLAG_ONE_CELL, (2, 3))])
+def test_cuda_graph_replay_same_bits(flags, tiles):
+    """Steps replayed from a CUDA graph (device step counter, dt log, latched
+    status) match the oracle bitwise in fixed and adaptive mode."""
+    cfg, ic, C = CASES["euler_random_300x200"]
+    W0 = ic()
+    ref = O.run(cfg, W0, 30, O.ADAPTIVE, C)
+    W, log = gpu_run(cfg, W0, 30, O.ADAPTIVE, C, flags=flags, tiles=tiles)
+    assert np.array_equal(log, ref.dt_log) and np.array_equal(W, ref.W)
+    s0, _ = O.smax(cfg, W0)
+    dt = 0.3 * (1.5 / 300) / s0
+    ref = O.run(cfg, W0, 20, O.FIXED, dt)
+    with solver_for(cfg, flags=flags, tiles=tiles) as s:
+        s.set_state(W0)
+        for _ in range(4):
+            s.step(dt, 5)
+        assert np.array_equal(s.get_state(), ref.W)
+        assert s.stats()["steps"] == 20
+
+
+def test_cuda_graph_error_latching_reports_the_step():
+    n = 64
+    cfg = O.Config(nx=n, ny=n, system=O.EULER, param=(G,))
+    W0 = inputs.euler_bell(n, n)
+    ref = O.run(cfg, W0, 400, O.FIXED, 1.0 * (1 / n) / 2.0, raise_on_error=False)
+    assert ref.status == O.E_CFL and ref.steps_done > 0
+    with solver_for(cfg, flags=fv2d.FLAG_GRAPH) as s:
+        s.set_state(W0)
+        s.step(1.0 * (1 / n) / 2.0, 400)
+        with pytest.raises(fv2d.FV2DError) as e:
+            s.synchronize()
+        assert e.value.code == fv2d.E_CFL and e.value.step == ref.steps_done
+        assert np.array_equal(s.get_state(raise_on_error=False), ref.W)
+
+
+def test_spray_tiled_and_graph():
+    cfg, W0, dt = spray_case(48)
+    ref = O.run(cfg, W0, 6, O.FIXED, dt)
+    for kw in (dict(tiles=(3, 4)), dict(flags=fv2d.FLAG_GRAPH), dict(flags=fv2d.FLAG_GRAPH, tiles=(2, 2))):
+        W, _ = gpu_run(cfg, W0, 6, O.FIXED, dt, **kw)
+        assert relerr(W, ref.W) <= 1e-10, kw
