@@ -198,6 +198,24 @@ fv2d_status fv2d_last_error(fv2d_ctx* ctx, char* buf, size_t n, int64_t* step, i
  * into step_kernel_ms. */
 fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out);
 
+/* Asynchronous output (the paper's gatherForOutput -> switch -> outputToDisk
+ * pipeline, which writes a snapshot without a global barrier):
+ * enqueue a copy of the current state W^k of this rank's slab into `host`
+ * (layout as fv2d_get_state; use fv2d_host_alloc memory for a truly
+ * asynchronous copy) and return at once.  On a side stream the state is
+ * converted into a device staging buffer and copied to the host while later
+ * steps run; only the step that would overwrite W^k's buffer waits for the
+ * conversion.  `host` must stay valid until fv2d_snapshot_wait returns.
+ * Snapshots are taken in call order; stepping results are unchanged (bitwise). */
+fv2d_status fv2d_snapshot(fv2d_ctx* ctx, double* host, fv2d_layout layout);
+
+/* Block until every enqueued snapshot has landed in host memory. */
+fv2d_status fv2d_snapshot_wait(fv2d_ctx* ctx);
+
+/* Page-locked host memory for snapshots / state transfers (cudaHostAlloc). */
+fv2d_status fv2d_host_alloc(size_t bytes, void** ptr);
+fv2d_status fv2d_host_free(void* ptr);
+
 /* enable != 0: record a CUDA event pair around every step-kernel launch (for the
  * roofline measurement of the dominant kernel); resets the accumulated time. */
 fv2d_status fv2d_set_profiling(fv2d_ctx* ctx, int32_t enable);

@@ -130,6 +130,11 @@ struct fv2d_ctx {
   double graph_dt = 0.0, graph_cfl = 0.0;
   bool graph_lam_valid = false;
   const double* graph_dt_log = nullptr;
+  // asynchronous output (fv2d_snapshot)
+  cudaStream_t out_stream = nullptr;
+  cudaEvent_t ev_snap_start = nullptr, ev_snap_conv = nullptr;
+  double* snap_buf = nullptr;
+  int snap_parity = -1;  // buffer being converted; the step that overwrites it must wait
   long long rs = 0;  // row stride (nv * pitch); a buffer holds rows -1..H
   double dx = 0, dy = 0, hmin = 0;
   // per local slab: two ping-pong buffers of (H+2) rows (ghost rows -1 and H inside)
@@ -585,6 +590,13 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   for (int p = 0; p < 2; ++p)
     if (ctx->graph[p]) cudaGraphExecDestroy(ctx->graph[p]);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->out_stream) {
+    cudaStreamSynchronize(ctx->out_stream);
+    cudaStreamDestroy(ctx->out_stream);
+  }
+  if (ctx->ev_snap_start) cudaEventDestroy(ctx->ev_snap_start);
+  if (ctx->ev_snap_conv) cudaEventDestroy(ctx->ev_snap_conv);
+  if (ctx->snap_buf) cudaFree(ctx->snap_buf);
   delete ctx;
   return FV2D_OK;
 }
@@ -750,6 +762,10 @@ static fv2d_status ensure_staging(fv2d_ctx* ctx) {
 
 static fv2d_status upload(fv2d_ctx* ctx, const double* src, fv2d_layout layout, cudaMemcpyKind kind) {
   CK(cudaSetDevice(ctx->cfg.device));
+  if (ctx->snap_parity >= 0) {
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_snap_conv, 0));
+    ctx->snap_parity = -1;
+  }
   const int nv = ctx->nv, nx = ctx->nx, H = ctx->H;
   if (layout == FV2D_SOA) {
     // SoA [nv][ny_local][nx]: per variable, slab rows are contiguous in the source
@@ -1018,6 +1034,10 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
   const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl;
   for (int32_t k = 0; k < nsteps; ++k) {
     const int p = cur_parity(ctx);
+    if (ctx->snap_parity == 1 - p) {  // this step writes the buffer a snapshot is reading
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_snap_conv, 0));
+      ctx->snap_parity = -1;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->profiling) {
       st = prof_events(ctx, &e0, &e1);
@@ -1141,6 +1161,64 @@ fv2d_status fv2d_set_profiling(fv2d_ctx* ctx, int32_t enable) {
   ctx->prof_ms = 0.0;
   ctx->prof_n = 0;
   return FV2D_OK;
+}
+
+fv2d_status fv2d_snapshot(fv2d_ctx* ctx, double* host, fv2d_layout layout) {
+  if (!ctx || !host || (layout != FV2D_AOS && layout != FV2D_SOA)) return FV2D_E_ARG;
+  if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int nv = ctx->nv, nx = ctx->nx, H = ctx->H;
+  const size_t bytes = (size_t)nv * nx * H * ctx->nslabs * sizeof(double);
+  if (!ctx->out_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_snap_start, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_snap_conv, cudaEventDisableTiming));
+    CK(cudaMalloc(&ctx->snap_buf, bytes));
+  }
+  if (ctx->snap_parity >= 0) {  // one conversion in flight at a time
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_snap_conv, 0));
+    ctx->snap_parity = -1;
+  }
+  const int p = cur_parity(ctx);
+  // "gather": convert W^k into the staging buffer on the side stream, after the
+  // work already queued on the main stream
+  CK(cudaEventRecord(ctx->ev_snap_start, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->out_stream, ctx->ev_snap_start, 0));
+  for (int s = 0; s < ctx->nslabs; ++s) {
+    if (layout == FV2D_AOS) {
+      dev_to_aos_kernel<<<148 * 4, 256, 0, ctx->out_stream>>>(row_ptr(ctx, s, p, 0),
+                                                              ctx->snap_buf + (size_t)s * H * nx * nv, nv, nx, H,
+                                                              ctx->pitch, ctx->rs);
+      CKL();
+    } else {
+      const long long nyl = (long long)H * ctx->nslabs;
+      for (int v = 0; v < nv; ++v)
+        CK(cudaMemcpy2DAsync(ctx->snap_buf + (size_t)v * nyl * nx + (size_t)s * H * nx, nx * sizeof(double),
+                             row_ptr(ctx, s, p, 0) + v * ctx->pitch, ctx->rs * sizeof(double), nx * sizeof(double),
+                             H, cudaMemcpyDeviceToDevice, ctx->out_stream));
+    }
+  }
+  CK(cudaEventRecord(ctx->ev_snap_conv, ctx->out_stream));
+  ctx->snap_parity = p;
+  // "outputToDisk" leg: device staging -> host, overlapped with later steps
+  CK(cudaMemcpyAsync(host, ctx->snap_buf, bytes, cudaMemcpyDeviceToHost, ctx->out_stream));
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_snapshot_wait(fv2d_ctx* ctx) {
+  if (!ctx) return FV2D_E_ARG;
+  if (ctx->out_stream) CK(cudaStreamSynchronize(ctx->out_stream));
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr || bytes == 0) return FV2D_E_ARG;
+  return cudaHostAlloc(ptr, bytes, cudaHostAllocDefault) == cudaSuccess ? FV2D_OK : FV2D_E_CUDA;
+}
+
+fv2d_status fv2d_host_free(void* ptr) {
+  if (!ptr) return FV2D_OK;
+  return cudaFreeHost(ptr) == cudaSuccess ? FV2D_OK : FV2D_E_CUDA;
 }
 
 fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out) {

@@ -70,11 +70,16 @@ def lib():
         L.fv2d_last_error.argtypes = [vp, C.c_char_p, C.c_size_t, P(C.c_int64), P(C.c_int64), d]
         L.fv2d_get_stats.argtypes = [vp, P(Stats)]
         L.fv2d_set_profiling.argtypes = [vp, C.c_int32]
+        L.fv2d_snapshot.argtypes = [vp, vp, C.c_int]
+        L.fv2d_snapshot_wait.argtypes = [vp]
+        L.fv2d_host_alloc.argtypes = [C.c_size_t, P(vp)]
+        L.fv2d_host_free.argtypes = [vp]
         for name in ("fv2d_version", "fv2d_config_default", "fv2d_nccl_unique_id", "fv2d_create", "fv2d_destroy",
                      "fv2d_set_state", "fv2d_set_state_device", "fv2d_get_state", "fv2d_compute_dt",
                      "fv2d_check_dt", "fv2d_step", "fv2d_step_adaptive", "fv2d_apply_source",
                      "fv2d_synchronize", "fv2d_device_state", "fv2d_last_error", "fv2d_get_stats",
-                     "fv2d_set_profiling"):
+                     "fv2d_set_profiling", "fv2d_snapshot", "fv2d_snapshot_wait", "fv2d_host_alloc",
+                     "fv2d_host_free"):
             getattr(L, name).restype = C.c_int
         _LIB = L
     return _LIB
@@ -110,6 +115,31 @@ def nccl_unique_id() -> bytes:
     if rc != OK:
         raise FV2DError(rc, "ncclGetUniqueId")
     return buf.raw
+
+
+class PinnedArray:
+    """A float64 numpy array in page-locked host memory (fv2d_host_alloc)."""
+
+    def __init__(self, shape):
+        n = int(np.prod(shape))
+        p = C.c_void_p()
+        rc = lib().fv2d_host_alloc(max(8, n * 8), C.byref(p))
+        if rc != OK:
+            raise FV2DError(rc, "fv2d_host_alloc")
+        self._p = p
+        self.array = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(n,)).reshape(shape)
+
+    def free(self):
+        if getattr(self, "_p", None):
+            self.array = None
+            lib().fv2d_host_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def _dp(a):
@@ -241,6 +271,17 @@ class Solver:
 
     def status(self) -> int:
         return lib().fv2d_synchronize(self._h)
+
+    def snapshot(self, out: "PinnedArray | np.ndarray", layout: int = AOS):
+        """Asynchronous copy of the current state into `out`; valid after
+        snapshot_wait().  Pass a PinnedArray for a copy that overlaps stepping."""
+        arr = out.array if isinstance(out, PinnedArray) else out
+        if arr.shape != self._shape(layout) or arr.dtype != np.float64 or not arr.flags.c_contiguous:
+            raise ValueError(f"snapshot buffer must be float64 C-contiguous {self._shape(layout)}")
+        self._check(lib().fv2d_snapshot(self._h, arr.ctypes.data, layout), "snapshot")
+
+    def snapshot_wait(self):
+        self._check(lib().fv2d_snapshot_wait(self._h), "snapshot_wait")
 
     def set_profiling(self, enable: bool = True):
         self._check(lib().fv2d_set_profiling(self._h, 1 if enable else 0), "set_profiling")

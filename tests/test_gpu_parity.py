@@ -397,3 +397,49 @@ def test_spray_tiled_and_graph():
     for kw in (dict(tiles=(3, 4)), dict(flags=fv2d.FLAG_GRAPH), dict(flags=fv2d.FLAG_GRAPH, tiles=(2, 2))):
         W, _ = gpu_run(cfg, W0, 6, O.FIXED, dt, **kw)
         assert relerr(W, ref.W) <= 1e-10, kw
+
+
+def test_async_output_changes_no_bit_and_snapshots_are_exact(tmp_path):
+    """SPEC criterion 5 / P:598-600: a 60-step run with an asynchronous output
+    every 20 steps gives the same final state bitwise, and each written file
+    holds exactly W^20, W^40, W^60."""
+    from paper_1701_05431_b200 import output
+    cfg, ic, C = CASES["euler_laxliu3_256"]
+    W0 = ic()
+    s0, _ = O.smax(cfg, W0)
+    dt = 0.4 * (1 / 256) / s0
+    ref = O.run(cfg, W0, 60, O.FIXED, dt, dump_steps=(20, 40, 60))
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        w = output.AsyncWriter(s, str(tmp_path / "snap_{step:03d}.tfv1"), nbuf=2)
+        t = 0.0
+        for k in range(60):
+            s.step(dt, 1)
+            t += dt
+            if (k + 1) % 20 == 0:
+                w.submit(k + 1, t)
+        paths = w.close()
+        final = s.get_state()
+    assert np.array_equal(final, ref.W)
+    assert len(paths) == 3
+    for k, p in zip((20, 40, 60), paths):
+        Wk, tk = output.read_tfv1(p)
+        assert np.array_equal(Wk, ref.dumps[k])
+
+
+def test_snapshot_soa_and_pinned():
+    cfg, ic, C = CASES["euler_random_300x200"]
+    W0 = ic()
+    ref = O.run(cfg, W0, 3, O.ADAPTIVE, C)
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        a = fv2d.PinnedArray((4, 200, 300))
+        b = np.empty((200, 300, 4))
+        s.snapshot(a, fv2d.SOA)
+        s.step_adaptive(C, 3, log=False)
+        s.snapshot(b, fv2d.AOS)
+        s.step_adaptive(C, 2, log=False)
+        s.snapshot_wait()
+        assert np.array_equal(a.array.transpose(1, 2, 0), W0)
+        assert np.array_equal(b, ref.W)
+        a.free()

@@ -49,3 +49,15 @@ def test_spray_ic_realizable():
     m0, m1, m2, m3 = (W[..., k] for k in range(4))
     assert np.all(m3 < m2) and np.all(m2 < m1) and np.all(m1 < m0)
     assert np.all(m1 * m1 < m0 * m2) and np.all(m2 * m2 < m1 * m3)
+
+
+def test_tfv1_roundtrip(tmp_path):
+    """SPEC's solution file: magic, LE int64 Nx Ny nVar, f64 t, data."""
+    from paper_1701_05431_b200 import output
+    W = inputs.euler_random(7, 5, seed=2)
+    p = tmp_path / "s.tfv1"
+    output.write_tfv1(str(p), W, 0.125)
+    raw = p.read_bytes()
+    assert raw[:4] == b"TFV1" and len(raw) == 4 + 32 + W.size * 8
+    W2, t = output.read_tfv1(str(p))
+    assert t == 0.125 and np.array_equal(W2, W)

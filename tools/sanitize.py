@@ -19,16 +19,27 @@ cases = [
          W=inputs.spray_taylor_green(33, 32)),
     dict(nx=100, ny=40, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_NAIVE, W=inputs.euler_random(100, 40)),
     dict(nx=100, ny=40, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_ONE_CELL, W=inputs.euler_random(100, 40)),
+    dict(nx=130, ny=60, system=fv2d.EULER, param=(1.4,), tiles=(3, 4), W=inputs.euler_random(130, 60)),
+    dict(nx=130, ny=60, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_GRAPH, tiles=(2, 2),
+         W=inputs.euler_random(130, 60)),
+    dict(nx=130, ny=64, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_NCCL_LOOPBACK, W=inputs.euler_random(130, 64)),
 ]
 for c in cases:
     W = c.pop("W")
+    if c.get("flags", 0) & fv2d.FLAG_NCCL_LOOPBACK:
+        c["nccl_id"] = fv2d.nccl_unique_id()
     with fv2d.Solver(**c) as s:
         s.set_state(W)
+        snap = fv2d.PinnedArray(W.shape)
+        s.snapshot(snap)
         s.step_adaptive(0.4, 3)
         dt, _ = s.compute_dt(0.4)
         s.step(dt * 0.9, 2)
         if c["system"] == fv2d.SPRAY:
             s.apply_source(1e-4)
         out = s.get_state()
+        s.snapshot_wait()
+        assert np.array_equal(snap.array, W)
+        snap.free()
         assert np.all(np.isfinite(out))
 print("sanitize cases ok")
