@@ -443,3 +443,43 @@ def test_snapshot_soa_and_pinned():
         assert np.array_equal(a.array.transpose(1, 2, 0), W0)
         assert np.array_equal(b, ref.W)
         a.free()
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    system = [O.ADVECTION, O.EULER, O.EULER][seed % 3]
+    nslabs = int(rng.choice([1, 1, 2, 3]))
+    ny = int(rng.integers(2, 40)) * nslabs
+    nx = int(rng.integers(3, 260))
+    bcs = [O.BC_PERIODIC, O.BC_DIRICHLET] + ([O.BC_WALL] if system != O.ADVECTION else [])
+    bc_x, bc_y = int(rng.choice(bcs)), int(rng.choice(bcs))
+    x1, y1 = float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 2.0))
+    if system == O.ADVECTION:
+        param = (float(rng.uniform(-2, 2)), float(rng.uniform(-2, 2)))
+        W0 = rng.normal(size=(ny, nx, 1))
+        dirichlet = (float(rng.normal()),)
+    else:
+        param = (float(rng.uniform(1.1, 1.7)),)
+        W0 = inputs.euler_random(nx, ny, seed=seed, gamma=param[0])
+        dirichlet = tuple(inputs.euler_random(1, 1, seed=seed + 7, gamma=param[0])[0, 0])
+    flags = int(rng.choice([0, 0, fv2d.FLAG_ONE_CELL, fv2d.FLAG_NAIVE, fv2d.FLAG_GRAPH]))
+    tiles = (1, 1)
+    if flags != fv2d.FLAG_NAIVE and rng.random() < 0.3 and nx >= 8:
+        tiles = (int(rng.integers(1, min(5, nx // 2) + 1)), int(rng.integers(1, min(4, ny // nslabs) + 1)))
+    cfg = O.Config(nx=nx, ny=ny, system=system, param=param, bc_x=bc_x, bc_y=bc_y, x1=x1, y1=y1,
+                   dirichlet=dirichlet)
+    return cfg, W0, dict(nslabs=nslabs, flags=flags, tiles=tiles), int(rng.integers(1, 12))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_randomized_configurations_bitwise(seed):
+    """Random mesh sizes (ragged, tiny), domains, systems, parameters, boundary
+    conditions, slab counts, kernels, tiles and graph mode: adaptive steps are
+    bitwise the oracle's."""
+    cfg, W0, kw, nsteps = _random_case(seed)
+    ref = O.run(cfg, W0, nsteps, O.ADAPTIVE, 0.4, raise_on_error=False)
+    if ref.status != O.OK:
+        pytest.skip(f"oracle status {ref.status} for this random state")
+    W, log = gpu_run(cfg, W0, nsteps, O.ADAPTIVE, 0.4, **kw)
+    assert np.array_equal(log, ref.dt_log), (cfg, kw)
+    assert np.array_equal(W, ref.W), (cfg, kw)
