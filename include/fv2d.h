@@ -80,6 +80,13 @@ typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
 #define FV2D_FLAG_GRAPH 0x20u      /* replay each step from a CUDA graph captured once per
                                         ping-pong parity (re-captured when dt/mode change);
                                         single-process contexts only */
+#define FV2D_FLAG_PEER_HALO 0x40u  /* nranks > 1 without NCCL: the step kernel stores its
+                                        boundary rows straight into the neighbours' ghost rows
+                                        over peer memory (NVLink), and the CFL max-all-reduce is
+                                        done with system-scope atomics and an arrival counter in
+                                        peer memory.  Connect with fv2d_peer_connect (CUDA IPC,
+                                        one process per GPU) or fv2d_peer_connect_local (ranks of
+                                        one process) before fv2d_set_state. */
 #define FV2D_FLAG_NCCL_LOOPBACK 0x8u /* take the NCCL halo/all-reduce path even with
                                         nranks == 1 (self send/recv; needs an id from
                                         fv2d_nccl_unique_id); exercises the multi-GPU
@@ -211,6 +218,21 @@ fv2d_status fv2d_snapshot(fv2d_ctx* ctx, double* host, fv2d_layout layout);
 
 /* Block until every enqueued snapshot has landed in host memory. */
 fv2d_status fv2d_snapshot_wait(fv2d_ctx* ctx);
+
+/* Peer-memory multi-GPU path (FV2D_FLAG_PEER_HALO).  fv2d_peer_export writes this
+ * rank's FV2D_PEER_HANDLE_BYTES of CUDA IPC handles (both state buffers and the
+ * collective sync block); gather them from every rank (rank-major) and pass the
+ * nranks * FV2D_PEER_HANDLE_BYTES bytes to fv2d_peer_connect on every rank.
+ * fv2d_peer_connect_local does the same for contexts of one process (group[r]
+ * = the context of rank r; the ranks must then be driven from separate host
+ * threads and streams, like separate processes).  Collective calls
+ * (set_state, compute_dt, check_dt, step*, apply_source) must be made by all
+ * ranks in the same order, as with NCCL; a rank that never arrives makes the
+ * others latch FV2D_E_NCCL after ~20 s instead of hanging. */
+#define FV2D_PEER_HANDLE_BYTES 192
+fv2d_status fv2d_peer_export(fv2d_ctx* ctx, uint8_t* handles);
+fv2d_status fv2d_peer_connect(fv2d_ctx* ctx, const uint8_t* all_handles);
+fv2d_status fv2d_peer_connect_local(fv2d_ctx* ctx, fv2d_ctx* const* group);
 
 /* Page-locked host memory for snapshots / state transfers (cudaHostAlloc). */
 fv2d_status fv2d_host_alloc(size_t bytes, void** ptr);

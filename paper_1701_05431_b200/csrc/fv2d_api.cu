@@ -155,6 +155,14 @@ struct fv2d_ctx {
   bool lam_valid = false;
   ncclComm_t comm = nullptr;
   bool use_nccl = false;  // nranks > 1, or FV2D_FLAG_NCCL_LOOPBACK (self exchange on 1 rank)
+  // FV2D_FLAG_PEER_HALO: halo rows and the CFL max-all-reduce through peer memory
+  bool peer = false, peer_connected = false;
+  PeerSync* sync = nullptr;               // own sync block
+  PeerArgs pa{};                          // every rank's sync block
+  double* peer_buf_s[2] = {nullptr, nullptr};  // south neighbour's buffers (parity 0/1)
+  double* peer_buf_n[2] = {nullptr, nullptr};  // north neighbour's buffers
+  std::vector<void*> ipc_opened;          // IPC mappings to close
+  unsigned long long epoch = 0;           // collective points issued so far
   cudaStream_t comm_stream = nullptr;  // NCCL halo exchange overlapped with the interior pass
   cudaEvent_t ev_bnd = nullptr, ev_int = nullptr, ev_fin = nullptr;
   // host state
@@ -226,7 +234,8 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   // south boundary row (row 0) -> south neighbour's north ghost row (row H)
   if (g > 0 || per) {
     const int gs_ = (g - 1 + G) % G;
-    if (!ctx->use_nccl && gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ghost_n(ctx, gs_ % ctx->nslabs, q);
+    if (ctx->peer) d.dst_s = ctx->peer_buf_s[q] ? ctx->peer_buf_s[q] + (long long)(ctx->H + 1) * ctx->rs : nullptr;
+    else if (!ctx->use_nccl && gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ghost_n(ctx, gs_ % ctx->nslabs, q);
     else d.dst_s = ctx->send_s;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
     d.dst_s = ghost_s(ctx, s, q);
@@ -235,7 +244,8 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   // north boundary row (row H-1) -> north neighbour's south ghost row (row -1)
   if (g < G - 1 || per) {
     const int gn_ = (g + 1) % G;
-    if (!ctx->use_nccl && gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ghost_s(ctx, gn_ % ctx->nslabs, q);
+    if (ctx->peer) d.dst_n = ctx->peer_buf_n[q];  // row -1 of the north neighbour's buffer
+    else if (!ctx->use_nccl && gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ghost_s(ctx, gn_ % ctx->nslabs, q);
     else d.dst_n = ctx->send_n;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
     d.dst_n = ghost_n(ctx, s, q);
@@ -313,6 +323,8 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.col_hi = ctx->nx;
   a.lam_cache = ctx->lam_cache;
   a.lam_valid = ctx->lam_valid ? 1 : 0;
+  a.peer_fence = ctx->peer ? 1 : 0;
+  if (ctx->peer) a.fused_finalize = 0;
   return a;
 }
 
@@ -427,6 +439,22 @@ fv2d_status allreduce_scalars(fv2d_ctx* ctx, cudaStream_t stream = nullptr) {
   return FV2D_OK;
 }
 
+// One collective point of the peer path: max-all-reduce dscal[0..1] -> dscal[4..5].
+fv2d_status peer_collective(fv2d_ctx* ctx, cudaStream_t stream) {
+  peer_collective_kernel<<<1, 32, 0, stream>>>(ctx->pa, ctx->dscal + 0, ctx->dscal + 4, ctx->epoch, ctx->dscal + 2);
+  ++ctx->epoch;
+  ++ctx->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ctx, FV2D_E_CUDA, "launch failed: %s", cudaGetErrorString(e));
+  return FV2D_OK;
+}
+
+// Cross-rank reduction of [smax, pending] after a local pass: NCCL or peer memory.
+fv2d_status reduce_ranks(fv2d_ctx* ctx, cudaStream_t stream) {
+  if (ctx->peer) return peer_collective(ctx, stream);
+  return allreduce_scalars(ctx, stream);
+}
+
 fv2d_status ensure_dt_log(fv2d_ctx* ctx, long long need) {
   if (need <= ctx->dt_log_cap) return FV2D_OK;
   long long cap = std::max<long long>(need, std::max<long long>(1024, 2 * ctx->dt_log_cap));
@@ -461,8 +489,8 @@ fv2d_status reduce_current(fv2d_ctx* ctx, double* smax_out, unsigned long long* 
   dispatch<LaunchReduce>(ctx->cfg.system, ctx, a);
   CKL();
   unsigned long long h[2];
-  if (ctx->use_nccl) {
-    fv2d_status s = allreduce_scalars(ctx);
+  if (ctx->use_nccl || ctx->peer) {
+    fv2d_status s = reduce_ranks(ctx, ctx->stream);
     if (s) return s;
     CK(cudaMemcpyAsync(h, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   } else {
@@ -491,6 +519,8 @@ fv2d_status report(fv2d_ctx* ctx, unsigned long long st) {
                      step, ctx->err_cell);
     case ST_NONFINITE:
       return set_err(ctx, FV2D_E_NONFINITE, "non-admissible state W^%lld (cell %lld)", step, ctx->err_cell);
+    case ST_COMM:
+      return set_err(ctx, FV2D_E_NCCL, "peer-memory collective timed out at epoch %lld (a rank did not arrive)", step);
     case ST_RECON:
       return set_err(ctx, FV2D_E_RECON, "NDF reconstruction failed in step %lld (cell %lld)", step, ctx->err_cell);
     default:
@@ -582,6 +612,8 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   if (ctx->trig) cudaFree(ctx->trig);
   if (ctx->lam_cache) cudaFree(ctx->lam_cache);
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (ctx->sync) cudaFree(ctx->sync);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
   if (ctx->ev_int) cudaEventDestroy(ctx->ev_int);
@@ -620,12 +652,16 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   const long long H = c.ny / (c.nranks * c.nslabs);
   if (H < 1) return FV2D_E_ARG;
   if (std::max(1, c.tiles_y) > H || 2 * std::max(1, c.tiles_x) > c.nx) return FV2D_E_ARG;
-  const bool use_nccl = c.nranks > 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK);
+  const bool peer = (c.flags & FV2D_FLAG_PEER_HALO) != 0;
+  if (peer && (c.nranks < 2 || c.nranks > kMaxRanks || c.nslabs != 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK)))
+    return FV2D_E_ARG;
+  const bool use_nccl = !peer && (c.nranks > 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK));
   if (use_nccl && (!nccl_id || !load_nccl())) return FV2D_E_NCCL;
 
   fv2d_ctx* ctx = new fv2d_ctx();
   ctx->cfg = c;
   ctx->use_nccl = use_nccl;
+  ctx->peer = peer;
   ctx->stream = (cudaStream_t)cuda_stream;
   ctx->launch_stream = ctx->stream;
   ctx->tiles_x = std::max(1, c.tiles_x);
@@ -674,6 +710,10 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     CKC(cudaMalloc(&ctx->send_n, row_bytes));
     CKC(cudaMemset(ctx->send_s, 0, row_bytes));
     CKC(cudaMemset(ctx->send_n, 0, row_bytes));
+  }
+  if (peer) {
+    CKC(cudaMalloc(&ctx->sync, sizeof(PeerSync)));
+    CKC(cudaMemset(ctx->sync, 0, sizeof(PeerSync)));
   }
   CKC(cudaMalloc(&ctx->dscal, 8 * sizeof(unsigned long long)));
   CKC(cudaMemset(ctx->dscal, 0, 8 * sizeof(unsigned long long)));
@@ -738,6 +778,12 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   fv2d_status st = exchange(ctx, 0);
   if (st) return st;
   unsigned long long init[8] = {0, 0, 0, ~0ull, 0, 0, 0, 0};
+  if (ctx->peer) {
+    // barrier: every rank has written its halo rows into its neighbours' ghost rows
+    CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    st = peer_collective(ctx, ctx->stream);
+    if (st) return st;
+  }
   CK(cudaMemcpyAsync(ctx->dscal, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->done, 0, sizeof(unsigned int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dt_dev, 0, sizeof(double), ctx->stream));
@@ -791,11 +837,13 @@ static fv2d_status upload(fv2d_ctx* ctx, const double* src, fv2d_layout layout, 
 
 fv2d_status fv2d_set_state(fv2d_ctx* ctx, const double* host, fv2d_layout layout) {
   if (!ctx || !host || (layout != FV2D_AOS && layout != FV2D_SOA)) return FV2D_E_ARG;
+  if (ctx->peer && !ctx->peer_connected) return set_err(ctx, FV2D_E_STATE, "peer halo: call fv2d_peer_connect first");
   return upload(ctx, host, layout, cudaMemcpyHostToDevice);
 }
 
 fv2d_status fv2d_set_state_device(fv2d_ctx* ctx, const double* dev, fv2d_layout layout) {
   if (!ctx || !dev || (layout != FV2D_AOS && layout != FV2D_SOA)) return FV2D_E_ARG;
+  if (ctx->peer && !ctx->peer_connected) return set_err(ctx, FV2D_E_STATE, "peer halo: call fv2d_peer_connect first");
   return upload(ctx, dev, layout, cudaMemcpyDeviceToDevice);
 }
 
@@ -985,7 +1033,14 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
     spray_source_dt_kernel_launch(ctx, b, grid, p);
     CKL();
   }
-  if (ctx->use_nccl) {
+  if (ctx->peer) {
+    // the halo rows are already in the neighbours' ghost rows (peer stores of
+    // the step kernel); reduce [smax, status] over the ranks through peer memory
+    st = peer_collective(ctx, ls);
+    if (st) return st;
+    finalize_kernel<<<1, 32, 0, ls>>>(a, ctx->dscal + 4);
+    CKL();
+  } else if (ctx->use_nccl) {
     st = exchange(ctx, 1 - p, ls);
     if (st) return st;
     st = allreduce_scalars(ctx, ls);
@@ -1031,7 +1086,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
   fv2d_status st = ensure_dt_log(ctx, ctx->steps + nsteps);
   if (st) return st;
   const bool split = ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE);
-  const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl;
+  const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl && !ctx->peer;
   for (int32_t k = 0; k < nsteps; ++k) {
     const int p = cur_parity(ctx);
     if (ctx->snap_parity == 1 - p) {  // this step writes the buffer a snapshot is reading
@@ -1108,7 +1163,14 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   ctx->lam_valid = true;
   fv2d_status st = exchange(ctx, p);
   if (st) return st;
-  promote_pending_kernel<<<1, 32, 0, ctx->stream>>>(ctx->dscal + 1, ctx->dscal + 2);
+  if (ctx->peer) {
+    st = peer_collective(ctx, ctx->stream);  // halo rows of all ranks in place + global status
+    if (st) return st;
+    CK(cudaMemsetAsync(ctx->dscal + 1, 0, sizeof(unsigned long long), ctx->stream));
+    promote_pending_kernel<<<1, 32, 0, ctx->stream>>>(ctx->dscal + 5, ctx->dscal + 2);
+  } else {
+    promote_pending_kernel<<<1, 32, 0, ctx->stream>>>(ctx->dscal + 1, ctx->dscal + 2);
+  }
   CKL();
   ctx->dt_valid = false;
   return FV2D_OK;
@@ -1219,6 +1281,94 @@ fv2d_status fv2d_host_alloc(size_t bytes, void** ptr) {
 fv2d_status fv2d_host_free(void* ptr) {
   if (!ptr) return FV2D_OK;
   return cudaFreeHost(ptr) == cudaSuccess ? FV2D_OK : FV2D_E_CUDA;
+}
+
+static fv2d_status peer_finish(fv2d_ctx* ctx) {
+  ctx->pa.nranks = ctx->cfg.nranks;
+  ctx->pa.me = ctx->cfg.rank;
+  ctx->pa.sync[ctx->cfg.rank] = ctx->sync;
+  ctx->peer_connected = true;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_peer_export(fv2d_ctx* ctx, uint8_t* out) {
+  if (!ctx || !out || !ctx->peer) return FV2D_E_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaIpcMemHandle_t h[3];
+  CK(cudaIpcGetMemHandle(&h[0], ctx->buf[0][0]));
+  CK(cudaIpcGetMemHandle(&h[1], ctx->buf[0][1]));
+  CK(cudaIpcGetMemHandle(&h[2], ctx->sync));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  memcpy(out, h, sizeof h);
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_peer_connect(fv2d_ctx* ctx, const uint8_t* all) {
+  if (!ctx || !all || !ctx->peer) return FV2D_E_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int P = ctx->cfg.nranks, r = ctx->cfg.rank;
+  const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
+  auto open = [&](int rank, int k, void** ptr) -> fv2d_status {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, all + (size_t)rank * FV2D_PEER_HANDLE_BYTES + (size_t)k * 64, 64);
+    CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->ipc_opened.push_back(*ptr);
+    return FV2D_OK;
+  };
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    void* p = nullptr;
+    fv2d_status st = open(q, 2, &p);
+    if (st) return st;
+    ctx->pa.sync[q] = (PeerSync*)p;
+  }
+  const int s_rank = (r > 0 || per) ? (r - 1 + P) % P : -1;
+  const int n_rank = (r < P - 1 || per) ? (r + 1) % P : -1;
+  void* bs[2] = {nullptr, nullptr};
+  void* bn[2] = {nullptr, nullptr};
+  for (int k = 0; k < 2; ++k) {
+    if (s_rank >= 0) {
+      fv2d_status st = open(s_rank, k, &bs[k]);
+      if (st) return st;
+    }
+    if (n_rank >= 0) {
+      if (n_rank == s_rank) bn[k] = bs[k];
+      else {
+        fv2d_status st = open(n_rank, k, &bn[k]);
+        if (st) return st;
+      }
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    ctx->peer_buf_s[k] = (double*)bs[k];
+    ctx->peer_buf_n[k] = (double*)bn[k];
+  }
+  return peer_finish(ctx);
+}
+
+fv2d_status fv2d_peer_connect_local(fv2d_ctx* ctx, fv2d_ctx* const* group) {
+  if (!ctx || !group || !ctx->peer) return FV2D_E_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int P = ctx->cfg.nranks, r = ctx->cfg.rank;
+  const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
+  for (int q = 0; q < P; ++q) {
+    if (!group[q] || group[q]->cfg.rank != q || group[q]->cfg.nranks != P || !group[q]->peer) return FV2D_E_ARG;
+    if (group[q]->cfg.device != ctx->cfg.device) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(group[q]->cfg.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return set_err(ctx, FV2D_E_CUDA, "peer access %d->%d: %s", ctx->cfg.device, group[q]->cfg.device,
+                       cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+    ctx->pa.sync[q] = group[q]->sync;
+  }
+  const int s_rank = (r > 0 || per) ? (r - 1 + P) % P : -1;
+  const int n_rank = (r < P - 1 || per) ? (r + 1) % P : -1;
+  for (int k = 0; k < 2; ++k) {
+    ctx->peer_buf_s[k] = s_rank >= 0 ? group[s_rank]->buf[0][k] : nullptr;
+    ctx->peer_buf_n[k] = n_rank >= 0 ? group[n_rank]->buf[0][k] : nullptr;
+  }
+  return peer_finish(ctx);
 }
 
 fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out) {

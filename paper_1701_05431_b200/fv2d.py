@@ -18,8 +18,9 @@ OK, E_ARG, E_CFL, E_NONFINITE, E_RECON, E_CUDA, E_NCCL, E_STATE = range(8)
 ADVECTION, EULER, SPRAY = 0, 1, 2
 BC_PERIODIC, BC_DIRICHLET, BC_WALL = 0, 1, 2
 AOS, SOA = 0, 1
-FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL, FLAG_NCCL_LOOPBACK, FLAG_FUSE_SOURCE, FLAG_GRAPH = (
-    0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
+FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL, FLAG_NCCL_LOOPBACK, FLAG_FUSE_SOURCE, FLAG_GRAPH, FLAG_PEER_HALO = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
+PEER_HANDLE_BYTES = 192
 NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
 _NAMES = {OK: "OK", E_ARG: "E_ARG", E_CFL: "E_CFL", E_NONFINITE: "E_NONFINITE", E_RECON: "E_RECON",
           E_CUDA: "E_CUDA", E_NCCL: "E_NCCL", E_STATE: "E_STATE"}
@@ -74,12 +75,15 @@ def lib():
         L.fv2d_snapshot_wait.argtypes = [vp]
         L.fv2d_host_alloc.argtypes = [C.c_size_t, P(vp)]
         L.fv2d_host_free.argtypes = [vp]
+        L.fv2d_peer_export.argtypes = [vp, C.c_char_p]
+        L.fv2d_peer_connect.argtypes = [vp, C.c_char_p]
+        L.fv2d_peer_connect_local.argtypes = [vp, P(vp)]
         for name in ("fv2d_version", "fv2d_config_default", "fv2d_nccl_unique_id", "fv2d_create", "fv2d_destroy",
                      "fv2d_set_state", "fv2d_set_state_device", "fv2d_get_state", "fv2d_compute_dt",
                      "fv2d_check_dt", "fv2d_step", "fv2d_step_adaptive", "fv2d_apply_source",
                      "fv2d_synchronize", "fv2d_device_state", "fv2d_last_error", "fv2d_get_stats",
                      "fv2d_set_profiling", "fv2d_snapshot", "fv2d_snapshot_wait", "fv2d_host_alloc",
-                     "fv2d_host_free"):
+                     "fv2d_host_free", "fv2d_peer_export", "fv2d_peer_connect", "fv2d_peer_connect_local"):
             getattr(L, name).restype = C.c_int
         _LIB = L
     return _LIB
@@ -282,6 +286,21 @@ class Solver:
 
     def snapshot_wait(self):
         self._check(lib().fv2d_snapshot_wait(self._h), "snapshot_wait")
+
+    # -- peer-memory multi-GPU path (FLAG_PEER_HALO)
+    def peer_export(self) -> bytes:
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        self._check(lib().fv2d_peer_export(self._h, buf), "peer_export")
+        return buf.raw
+
+    def peer_connect(self, all_handles: bytes):
+        """all_handles: every rank's peer_export() bytes, concatenated in rank order."""
+        self._check(lib().fv2d_peer_connect(self._h, all_handles), "peer_connect")
+
+    def peer_connect_local(self, group):
+        """group[r]: the Solver of rank r, all in this process (drive them from separate threads)."""
+        arr = (C.c_void_p * len(group))(*[g._h.value for g in group])
+        self._check(lib().fv2d_peer_connect_local(self._h, arr), "peer_connect_local")
 
     def set_profiling(self, enable: bool = True):
         self._check(lib().fv2d_set_profiling(self._h, 1 if enable else 0), "set_profiling")

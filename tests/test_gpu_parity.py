@@ -483,3 +483,61 @@ def test_randomized_configurations_bitwise(seed):
     W, log = gpu_run(cfg, W0, nsteps, O.ADAPTIVE, 0.4, **kw)
     assert np.array_equal(log, ref.dt_log), (cfg, kw)
     assert np.array_equal(W, ref.W), (cfg, kw)
+
+
+def _peer_group_run(cfg, W0, P, nsteps, mode, value, flags=0):
+    """P ranks of the peer-memory path as contexts of this process on one GPU,
+    each driven by its own host thread and stream (like separate processes)."""
+    import threading
+
+    import torch
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    H = cfg.ny // P
+    solvers = [solver_for(cfg, rank=r, nranks=P, flags=fv2d.FLAG_PEER_HALO | flags,
+                          stream=streams[r].cuda_stream) for r in range(P)]
+    for s in solvers:
+        s.peer_connect_local(solvers)
+    out, logs, errs = [None] * P, [None] * P, []
+
+    def work(r):
+        try:
+            s = solvers[r]
+            s.set_state(W0[r * H:(r + 1) * H])
+            if mode == O.ADAPTIVE:
+                logs[r] = s.step_adaptive(value, nsteps)
+            else:
+                s.step(value, nsteps)
+            out[r] = s.get_state()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for s in solvers:
+        s.close()
+    assert not errs, errs
+    return np.concatenate(out, axis=0), logs
+
+
+@pytest.mark.parametrize("P,bc_y", [(2, O.BC_PERIODIC), (3, O.BC_PERIODIC), (4, O.BC_WALL), (2, O.BC_WALL)])
+def test_peer_memory_halo_and_allreduce_bitwise(P, bc_y):
+    """FV2D_FLAG_PEER_HALO: boundary rows stored by the step kernel straight into
+    the neighbours' ghost rows, CFL max-all-reduce through peer-memory atomics and
+    an arrival counter -- no NCCL.  Same bits and dt sequence as the oracle."""
+    cfg = O.Config(nx=150, ny=96, system=O.EULER, param=(G,), bc_y=bc_y)
+    W0 = inputs.euler_random(150, 96, seed=40 + P)
+    ref = O.run(cfg, W0, 25, O.ADAPTIVE, 0.45)
+    W, logs = _peer_group_run(cfg, W0, P, 25, O.ADAPTIVE, 0.45)
+    for lg in logs:
+        assert np.array_equal(lg, ref.dt_log)
+    assert np.array_equal(W, ref.W)
+
+
+def test_peer_memory_spray_and_fixed_dt():
+    cfg, W0, dt = spray_case(48)
+    ref = O.run(cfg, W0, 5, O.FIXED, dt)
+    W, _ = _peer_group_run(cfg, W0, 2, 5, O.FIXED, dt)
+    assert relerr(W, ref.W) <= 1e-10
