@@ -258,9 +258,10 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
 // to 4 rows for small ones, where the serial march of a strip (latency), not
 // bandwidth, bounds the launch.
 int pick_rps(int ncols, int nrows) {
+  static const int rps_max = getenv("FV2D_RPS_MAX") ? atoi(getenv("FV2D_RPS_MAX")) : 128;  // tuning knob
   const long long colblocks = ((ncols + 62) / 62 + kWarps - 1) / kWarps;
   const long long rps = colblocks * nrows / (148 * 6);
-  return (int)std::max<long long>(4, std::min<long long>(128, rps));
+  return (int)std::max<long long>(4, std::min<long long>(rps_max, rps));
 }
 
 // Row ranges of a marching-kernel launch (see StepArgs).
@@ -459,12 +460,13 @@ fv2d_status ensure_dt_log(fv2d_ctx* ctx, long long need) {
   if (need <= ctx->dt_log_cap) return FV2D_OK;
   long long cap = std::max<long long>(need, std::max<long long>(1024, 2 * ctx->dt_log_cap));
   double* nb = nullptr;
-  CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaMalloc(&nb, cap * sizeof(double)));
-  CK(cudaMemset(nb, 0, cap * sizeof(double)));
+  // stream-ordered: no legacy-stream or device-wide synchronisation while
+  // stepping (ranks of a peer group may be waiting on this one's progress)
+  CK(cudaMallocAsync(&nb, cap * sizeof(double), ctx->stream));
+  CK(cudaMemsetAsync(nb, 0, cap * sizeof(double), ctx->stream));
   if (ctx->dt_log) {
-    CK(cudaMemcpy(nb, ctx->dt_log, ctx->dt_log_cap * sizeof(double), cudaMemcpyDeviceToDevice));
-    CK(cudaFree(ctx->dt_log));
+    CK(cudaMemcpyAsync(nb, ctx->dt_log, ctx->dt_log_cap * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaFreeAsync(ctx->dt_log, ctx->stream));
   }
   ctx->dt_log = nb;
   ctx->dt_log_cap = cap;
@@ -511,7 +513,8 @@ fv2d_status report(fv2d_ctx* ctx, unsigned long long st) {
   const long long step = (long long)(st & 0x00FFFFFFFFFFFFFFull);
   ctx->err_step = step;
   unsigned long long bc = ~0ull;
-  cudaMemcpy(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost);
+  if (cudaMemcpyAsync(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess)
+    cudaStreamSynchronize(ctx->stream);
   ctx->err_cell = bc == ~0ull ? -1 : (long long)bc;
   switch (code) {
     case ST_CFL:
@@ -722,6 +725,9 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   CKC(cudaMemset(ctx->done, 0, sizeof(unsigned int)));
   CKC(cudaMalloc(&ctx->dt_dev, sizeof(double)));
   CKC(cudaMemset(ctx->dt_dev, 0, sizeof(double)));
+  ctx->dt_log_cap = 1 << 16;  // grown stream-ordered by ensure_dt_log if a run is longer
+  CKC(cudaMalloc(&ctx->dt_log, ctx->dt_log_cap * sizeof(double)));
+  CKC(cudaMemset(ctx->dt_log, 0, ctx->dt_log_cap * sizeof(double)));
   CKC(cudaMalloc(&ctx->newton, sizeof(unsigned long long)));
   CKC(cudaMemset(ctx->newton, 0, sizeof(unsigned long long)));
   if (c.system == FV2D_SPRAY) {
@@ -799,9 +805,9 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
 static fv2d_status ensure_staging(fv2d_ctx* ctx) {
   const size_t need = (size_t)ctx->nv * ctx->nx * ctx->H * ctx->nslabs * sizeof(double);
   if (ctx->staging_bytes >= need) return FV2D_OK;
-  if (ctx->staging) CK(cudaFree(ctx->staging));
+  if (ctx->staging) CK(cudaFreeAsync(ctx->staging, ctx->stream));
   ctx->staging = nullptr;
-  CK(cudaMalloc(&ctx->staging, need));
+  CK(cudaMallocAsync(&ctx->staging, need, ctx->stream));
   ctx->staging_bytes = need;
   return FV2D_OK;
 }
@@ -1202,7 +1208,8 @@ fv2d_status fv2d_last_error(fv2d_ctx* ctx, char* buf, size_t n, int64_t* step, i
     report(ctx, st);
     diagnose(ctx, st);
     unsigned long long bc = ~0ull;
-    cudaMemcpy(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost);
+    if (cudaMemcpyAsync(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess)
+      cudaStreamSynchronize(ctx->stream);
     ctx->err_cell = bc == ~0ull ? -1 : (long long)bc;
   }
   if (buf && n) {
@@ -1235,7 +1242,7 @@ fv2d_status fv2d_snapshot(fv2d_ctx* ctx, double* host, fv2d_layout layout) {
     CK(cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_snap_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_snap_conv, cudaEventDisableTiming));
-    CK(cudaMalloc(&ctx->snap_buf, bytes));
+    CK(cudaMallocAsync(&ctx->snap_buf, bytes, ctx->stream));
   }
   if (ctx->snap_parity >= 0) {  // one conversion in flight at a time
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_snap_conv, 0));
@@ -1380,10 +1387,11 @@ fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out) {
   out->steps = ctx->steps;
   out->kernel_launches = ctx->launches;
   unsigned long long ni = 0;
-  if (ctx->newton) cudaMemcpy(&ni, ctx->newton, sizeof ni, cudaMemcpyDeviceToHost);
+  if (ctx->newton) cudaMemcpyAsync(&ni, ctx->newton, sizeof ni, cudaMemcpyDeviceToHost, ctx->stream);
   out->newton_iters = (int64_t)ni;
   double d = 0;
-  if (ctx->dt_dev) cudaMemcpy(&d, ctx->dt_dev, sizeof d, cudaMemcpyDeviceToHost);
+  if (ctx->dt_dev) cudaMemcpyAsync(&d, ctx->dt_dev, sizeof d, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
   out->dt = d;
   return FV2D_OK;
 }
