@@ -48,7 +48,7 @@ def lib():
     """Load libfv2d.so (building it in-tree first if missing or stale)."""
     global _LIB
     if _LIB is None:
-        path = _build.build()
+        path = os.environ.get("FV2D_LIB") or _build.build()  # FV2D_LIB: an alternative build (tuning)
         L = C.CDLL(path)
         P = C.POINTER
         vp = C.c_void_p

@@ -541,3 +541,36 @@ def test_peer_memory_spray_and_fixed_dt():
     ref = O.run(cfg, W0, 5, O.FIXED, dt)
     W, _ = _peer_group_run(cfg, W0, 2, 5, O.FIXED, dt)
     assert relerr(W, ref.W) <= 1e-10
+
+
+def test_c2_full_size_1024_lax_liu_100_steps():
+    """BASELINE configs[1] at its full size: 1024^2 Lax-Liu 3, 100 adaptive steps,
+    bitwise with an identical dt sequence."""
+    n = 1024
+    cfg = O.Config(nx=n, ny=n, system=O.EULER, param=(G,))
+    W0 = inputs.euler_lax_liu3(n, n)
+    ref = O.run(cfg, W0, 100, O.ADAPTIVE, 0.45)
+    W, log = gpu_run(cfg, W0, 100, O.ADAPTIVE, 0.45)
+    assert np.array_equal(log, ref.dt_log)
+    assert relerr(W, ref.W) <= 1e-10
+    assert np.array_equal(W, ref.W)
+
+
+def test_c4_full_size_4096_spray_sampled_rows():
+    """BASELINE configs[3] at full size (4096^2 spray, R16 IC, fixed dt R17) in
+    the default launch configuration: one step, sampled row bands recomputed by
+    the oracle (transport is stencil-local, the source cell-local): <= 1e-12."""
+    n = 4096
+    cfg = O.Config(nx=n, ny=n, system=O.SPRAY, param=(1.0, 1.0))
+    W0 = inputs.spray_taylor_green(n, n)
+    s0, _ = O.smax(cfg, W0)
+    dt = 0.5 * (1.0 / n) / s0
+    W1, _ = gpu_run(cfg, W0, 1, O.FIXED, dt)
+    for j0 in (0, 1500, 4090):
+        rows = [r % n for r in range(j0 - 1, j0 + 7)]
+        bcfg = O.Config(nx=n, ny=len(rows), system=O.SPRAY, param=(1.0, 1.0), y0=(j0 - 1) / n,
+                        y1=(j0 - 1 + len(rows)) / n)
+        band = O.transport_step(bcfg, W0[rows], dt)
+        band, _ = O.source_step(bcfg, band, dt)
+        got = W1[[r % n for r in range(j0, j0 + 6)]]
+        assert relerr(got, band[1:-1]) <= 1e-12
