@@ -19,8 +19,8 @@ def nccl_include() -> str:
     return os.path.join(base, "include")
 
 
-def nvcc_cmd(out: str, verbose_ptxas: bool = False) -> list[str]:
-    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+def nvcc_cmd(out: str, verbose_ptxas: bool = False, defines=()) -> list[str]:
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", *[f"-D{d}" for d in defines],
            "--fmad=false",                 # exact build: no FMA contraction
            "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-I", os.path.join(ROOT, "include"), "-I", nccl_include(),
@@ -37,20 +37,22 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libfv2d.so (or, with `out`, a tuning variant with extra -D defines)."""
+    target = out or LIB
+    if out is None and not force and not stale():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = nvcc_cmd(tmp, verbose)
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    tmp = target + f".tmp{os.getpid()}"
+    cmd = nvcc_cmd(tmp, verbose, defines)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libfv2d.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
