@@ -961,7 +961,7 @@ static fv2d_status prof_events(fv2d_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1) 
 static void spray_source_dt_kernel_launch(fv2d_ctx* ctx, const StepArgs& a, dim3 grid, int p) {
   StepArgs b = a;
   for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, 1 - p, 0);
-  spray_source_step_kernel<<<grid, 128, 0, ctx->launch_stream>>>(b);
+  spray_source_step_kernel<<<grid, kSrcThreads, 0, ctx->launch_stream>>>(b);
 }
 
 // The launches of one time step reading parity p, on ctx->launch_stream (the
@@ -1033,7 +1033,7 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
   if (split) {
     // in place on the transport output; dt: the fixed dt, or read from the
     // device in adaptive mode (the finalize writes dt_{n+1} only after this pass)
-    dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
+    dim3 grid((ctx->nx + kSrcThreads - 1) / kSrcThreads, std::min(ctx->H, 65535), ctx->nslabs);
     StepArgs b = a;
     if (tiled) b.fused_finalize = 0;
     spray_source_dt_kernel_launch(ctx, b, grid, p);
@@ -1163,8 +1163,8 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   StepArgs b = make_args(ctx, 1 - p);
   for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, p, 0);
   b.step = ctx->steps;
-  dim3 grid((ctx->nx + 127) / 128, std::min(ctx->H, 65535), ctx->nslabs);
-  spray_source_kernel<<<grid, 128, 0, ctx->stream>>>(b, dt, 0);
+  dim3 grid((ctx->nx + kSrcThreads - 1) / kSrcThreads, std::min(ctx->H, 65535), ctx->nslabs);
+  spray_source_kernel<<<grid, kSrcThreads, 0, ctx->stream>>>(b, dt, 0);
   CKL();
   ctx->lam_valid = true;
   fv2d_status st = exchange(ctx, p);
