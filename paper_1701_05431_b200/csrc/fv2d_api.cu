@@ -260,6 +260,8 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
 int pick_rps(int ncols, int nrows) {
   static const int rps_max = getenv("FV2D_RPS_MAX") ? atoi(getenv("FV2D_RPS_MAX")) : 128;  // tuning knob
   const long long colblocks = ((ncols + 62) / 62 + kWarps - 1) / kWarps;
+  static const int rps_force = getenv("FV2D_RPS") ? atoi(getenv("FV2D_RPS")) : 0;  // tuning knob
+  if (rps_force > 0) return std::min(rps_force, std::max(1, nrows));
   const long long rps = colblocks * nrows / (148 * 6);
   return (int)std::max<long long>(4, std::min<long long>(rps_max, rps));
 }

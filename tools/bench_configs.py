@@ -72,6 +72,9 @@ if __name__ == "__main__":
         W = euler_ic(1024)
         run("c2_euler_1024", fv2d.EULER, 1024, W, 100, 5)
         run("c2_euler_1024_adaptive", fv2d.EULER, 1024, W, 100, 5, adaptive=True)
+        run("c2_euler_1024_naive", fv2d.EULER, 1024, W, 100, 5, flags=fv2d.FLAG_NAIVE)
+        run("c2_euler_1024_onecell", fv2d.EULER, 1024, W, 100, 5, flags=fv2d.FLAG_ONE_CELL)
+        run("c2_euler_1024_graph", fv2d.EULER, 1024, W, 100, 5, flags=fv2d.FLAG_GRAPH)
     if want("c3"):
         W = euler_ic(16384)
         run("c3_euler_16384_pair", fv2d.EULER, 16384, W, 50, 3)
