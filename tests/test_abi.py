@@ -61,3 +61,22 @@ def test_create_validates_before_touching_the_device():
     assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
     assert L.fv2d_step(None, 1e-3, 1) == fv2d.E_ARG
     assert L.fv2d_destroy(None) == fv2d.OK
+
+
+def test_c_client_compiles_against_the_header():
+    """The ABI is usable from plain C (examples/c_client.c): header + .so only."""
+    exe = os.path.join(ROOT, "examples", "c_client")
+    r = subprocess.run(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "c_client.c"), "-L", os.path.dirname(fv2d.lib_path()),
+                        "-lfv2d", f"-Wl,-rpath,{os.path.dirname(fv2d.lib_path())}", "-lm", "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_c_client_runs():
+    exe = os.path.join(ROOT, "examples", "c_client")
+    test_c_client_compiles_against_the_header()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "c_client ok" in r.stdout
