@@ -30,7 +30,11 @@
  *  - Layouts: FV2D_AOS is the paper's Cell array: double
  *    W[ny][nx][nvar] (x fastest, variable innermost).  FV2D_SOA is
  *    double W[nvar][ny][nx].  With nranks > 1 every host array holds this
- *    rank's slab only: rows [rank*ny/nranks, (rank+1)*ny/nranks).
+ *    rank's block only: with y-slabs (nranks_x <= 1) rows
+ *    [rank*ny/nranks, (rank+1)*ny/nranks) of all nx columns; with 2-D blocks
+ *    (nranks_x = PX > 1, PY = nranks/PX, rank = ry*PX + rx) rows
+ *    [ry*ny/PY, (ry+1)*ny/PY) x columns [rx*nx/PX, (rx+1)*nx/PX), so nx and ny
+ *    in the shapes above read as the block's width and height.
  */
 #ifndef FV2D_H
 #define FV2D_H
@@ -91,6 +95,13 @@ typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
                                         nranks == 1 (self send/recv; needs an id from
                                         fv2d_nccl_unique_id); exercises the multi-GPU
                                         plumbing on one device */
+#define FV2D_FLAG_GHOST_COLUMNS 0x80u /* store x-ghost columns and route the x-neighbour data
+                                        through them exactly as for 2-D rank blocks
+                                        (nranks_x > 1, where this is implied), even with
+                                        one block along x: that block is its own west/east
+                                        neighbour when x is periodic.  Same bits; with
+                                        FV2D_FLAG_NCCL_LOOPBACK it exercises the NCCL column
+                                        exchange (pack, send/recv, unpack) on one device */
 
 typedef struct {
   int32_t nx, ny;          /* global mesh, >= 1; ny % (nranks*nslabs) == 0 */
@@ -109,7 +120,14 @@ typedef struct {
                               tiles_x x tiles_y separate sub-launches over the slab (the
                               paper's NPartX x NPartY task decomposition, P:215-220;
                               granularity study P:741-754).  Same bits. */
-  int32_t reserved[5];     /* must be 0 */
+  int32_t nranks_x;        /* 0/1: y-slabs.  PX > 1: the ranks form a PX x (nranks/PX) grid of
+                              2-D blocks (the paper's NPartX x NPartY decomposition with
+                              its four overlaps): rank = ry*PX + rx owns
+                              columns [rx*nx/PX, ...) of rows [ry*ny/PY, ...); each block
+                              also stores its east/west ghost columns, written by the
+                              neighbours' step kernels (FV2D_FLAG_PEER_HALO) or exchanged
+                              by NCCL.  Requires nx % PX == 0, nx/PX >= 2, nslabs == 1. */
+  int32_t reserved[4];     /* must be 0 */
 } fv2d_config;
 
 typedef struct fv2d_ctx fv2d_ctx;

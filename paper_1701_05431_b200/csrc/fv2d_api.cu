@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -119,6 +121,11 @@ struct fv2d_ctx {
   fv2d_config cfg{};
   cudaStream_t stream = nullptr;
   int nv = 0, nx = 0, H = 0, pitch = 0, nslabs = 1, G = 1, rps = 64;
+  // rank grid: px x py blocks, rank = ry * px + rx (px = 1: y-slabs).  nx is the
+  // local block width; gnx the global one; col0 the block's first global column;
+  // xoff the row-base offset that makes room for the ghost columns (px > 1).
+  int px = 1, py = 1, rx = 0, ry = 0, gnx = 0, col0 = 0, xoff = 0;
+  bool xg = false;  // stored ghost columns: px > 1 or FV2D_FLAG_GHOST_COLUMNS
   int ring_depth = 4;  // rows in the pair kernel's per-warp prefetch ring
   int tiles_x = 1, tiles_y = 1;  // launch decomposition of a step (granularity study)
   cudaStream_t launch_stream = nullptr;  // stream kernels are launched on (capture stream while capturing)
@@ -141,6 +148,10 @@ struct fv2d_ctx {
   double* buf[kMaxSlabs][2] = {};
   double* send_s = nullptr;  // nranks > 1: boundary rows to send
   double* send_n = nullptr;
+  double* send_w = nullptr;  // px > 1 (NCCL): packed boundary columns [H][nv] to send
+  double* send_e = nullptr;
+  double* recv_w = nullptr;  // ... and received, unpacked into the ghost columns
+  double* recv_e = nullptr;
   double* staging = nullptr;
   size_t staging_bytes = 0;
   // device scalars
@@ -161,6 +172,8 @@ struct fv2d_ctx {
   PeerArgs pa{};                          // every rank's sync block
   double* peer_buf_s[2] = {nullptr, nullptr};  // south neighbour's buffers (parity 0/1)
   double* peer_buf_n[2] = {nullptr, nullptr};  // north neighbour's buffers
+  double* peer_buf_w[2] = {nullptr, nullptr};  // west / east neighbours' buffers (px > 1)
+  double* peer_buf_e[2] = {nullptr, nullptr};
   std::vector<void*> ipc_opened;          // IPC mappings to close
   unsigned long long epoch = 0;           // collective points issued so far
   cudaStream_t comm_stream = nullptr;  // NCCL halo exchange overlapped with the interior pass
@@ -217,13 +230,19 @@ fv2d_status set_err(fv2d_ctx* c, fv2d_status st, const char* fmt, ...) {
     if (e_ != cudaSuccess) return set_err(ctx, FV2D_E_CUDA, "launch failed: %s", cudaGetErrorString(e_)); \
   } while (0)
 
-double* row_ptr(const fv2d_ctx* ctx, int s, int p, int j) { return ctx->buf[s][p] + (long long)(j + 1) * ctx->rs; }
+double* row_ptr(const fv2d_ctx* ctx, int s, int p, int j) {
+  return ctx->buf[s][p] + (long long)(j + 1) * ctx->rs + ctx->xoff;
+}
+// Rank of the block at grid position (x, y), with wrap.
+int rank_at(const fv2d_ctx* ctx, int x, int y) {
+  return ((y + ctx->py) % ctx->py) * ctx->px + (x + ctx->px) % ctx->px;
+}
 double* ghost_s(const fv2d_ctx* ctx, int s, int p) { return row_ptr(ctx, s, p, -1); }
 double* ghost_n(const fv2d_ctx* ctx, int s, int p) { return row_ptr(ctx, s, p, ctx->H); }
 
 // Ghost targets of local slab s for writes landing in ghost rows of parity q.
 void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
-  const int g = ctx->cfg.rank * ctx->nslabs + s;
+  const int g = ctx->ry * ctx->nslabs + s;
   const int G = ctx->G;
   const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
   const int my_y = nvar_of(ctx->cfg.system) == 4 ? 2 : (nvar_of(ctx->cfg.system) == 6 ? 5 : -1);
@@ -234,9 +253,10 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   // south boundary row (row 0) -> south neighbour's north ghost row (row H)
   if (g > 0 || per) {
     const int gs_ = (g - 1 + G) % G;
-    if (ctx->peer) d.dst_s = ctx->peer_buf_s[q] ? ctx->peer_buf_s[q] + (long long)(ctx->H + 1) * ctx->rs : nullptr;
-    else if (!ctx->use_nccl && gs_ / ctx->nslabs == ctx->cfg.rank) d.dst_s = ghost_n(ctx, gs_ % ctx->nslabs, q);
-    else d.dst_s = ctx->send_s;
+    if (ctx->peer)
+      d.dst_s = ctx->peer_buf_s[q] ? ctx->peer_buf_s[q] + (long long)(ctx->H + 1) * ctx->rs + ctx->xoff : nullptr;
+    else if (!ctx->use_nccl && gs_ / ctx->nslabs == ctx->ry) d.dst_s = ghost_n(ctx, gs_ % ctx->nslabs, q);
+    else d.dst_s = ctx->send_s + ctx->xoff;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
     d.dst_s = ghost_s(ctx, s, q);
     d.mirror_s = my_y;
@@ -244,12 +264,52 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   // north boundary row (row H-1) -> north neighbour's south ghost row (row -1)
   if (g < G - 1 || per) {
     const int gn_ = (g + 1) % G;
-    if (ctx->peer) d.dst_n = ctx->peer_buf_n[q];  // row -1 of the north neighbour's buffer
-    else if (!ctx->use_nccl && gn_ / ctx->nslabs == ctx->cfg.rank) d.dst_n = ghost_s(ctx, gn_ % ctx->nslabs, q);
-    else d.dst_n = ctx->send_n;
+    if (ctx->peer) d.dst_n = ctx->peer_buf_n[q] ? ctx->peer_buf_n[q] + ctx->xoff : nullptr;  // its row -1
+    else if (!ctx->use_nccl && gn_ / ctx->nslabs == ctx->ry) d.dst_n = ghost_s(ctx, gn_ % ctx->nslabs, q);
+    else d.dst_n = ctx->send_n + ctx->xoff;
   } else if (ctx->cfg.bc_y == FV2D_BC_WALL) {
     d.dst_n = ghost_n(ctx, s, q);
     d.mirror_n = my_y;
+  }
+  // 2-D rank blocks: column 0 -> west neighbour's ghost column nx, column nx-1
+  // -> east neighbour's ghost column -1 (same row layout on every rank); at a
+  // global wall, this buffer's own ghost column, mirrored (R13)
+  d.dst_w = d.dst_e = nullptr;
+  d.mirror_w = d.mirror_e = -1;
+  d.csr_w = d.csr_e = ctx->rs;
+  d.csv_w = d.csv_e = ctx->pitch;
+  if (ctx->xg) {
+    const bool perx = ctx->cfg.bc_x == FV2D_BC_PERIODIC;
+    const int my_x = nvar_of(ctx->cfg.system) == 4 ? 1 : (nvar_of(ctx->cfg.system) == 6 ? 4 : -1);
+    double* own0 = row_ptr(ctx, s, q, 0);
+    if (ctx->rx > 0 || perx) {
+      if (ctx->peer) {
+        d.dst_w = ctx->peer_buf_w[q] ? ctx->peer_buf_w[q] + ctx->rs + ctx->xoff + ctx->nx : nullptr;
+      } else if (!ctx->use_nccl) {
+        d.dst_w = own0 + ctx->nx;  // one block along x (px = 1): its own east ghost column
+      } else {
+        d.dst_w = ctx->send_w;
+        d.csr_w = ctx->nv;
+        d.csv_w = 1;
+      }
+    } else if (ctx->cfg.bc_x == FV2D_BC_WALL) {
+      d.dst_w = own0 - 1;
+      d.mirror_w = my_x;
+    }
+    if (ctx->rx < ctx->px - 1 || perx) {
+      if (ctx->peer) {
+        d.dst_e = ctx->peer_buf_e[q] ? ctx->peer_buf_e[q] + ctx->rs + ctx->xoff - 1 : nullptr;
+      } else if (!ctx->use_nccl) {
+        d.dst_e = own0 - 1;
+      } else {
+        d.dst_e = ctx->send_e;
+        d.csr_e = ctx->nv;
+        d.csv_e = 1;
+      }
+    } else if (ctx->cfg.bc_x == FV2D_BC_WALL) {
+      d.dst_e = own0 + ctx->nx;
+      d.mirror_e = my_x;
+    }
   }
 }
 
@@ -288,7 +348,7 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
     d.in = row_ptr(ctx, s, p, 0);
     d.out = row_ptr(ctx, s, q, 0);
     ghost_targets(ctx, s, q, d);
-    d.row0 = (ctx->cfg.rank * ctx->nslabs + s) * ctx->H;
+    d.row0 = (ctx->ry * ctx->nslabs + s) * ctx->H;
     d.H = ctx->H;
   }
   a.nx = ctx->nx;
@@ -314,11 +374,11 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.done = ctx->done;
   a.fused_finalize = ctx->use_nccl ? 0 : 1;
   a.fuse_source = (ctx->cfg.system == FV2D_SPRAY && (ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE)) ? 1 : 0;
-  if (ctx->trig) {
-    a.sx_tab = ctx->trig;
-    a.cx_tab = ctx->trig + ctx->nx;
-    a.sy_tab = ctx->trig + 2 * ctx->nx;
-    a.cy_tab = ctx->trig + 2 * ctx->nx + ctx->cfg.ny;
+  if (ctx->trig) {  // tables over the global mesh; x tables offset to this block
+    a.sx_tab = ctx->trig + ctx->col0;
+    a.cx_tab = ctx->trig + ctx->gnx + ctx->col0;
+    a.sy_tab = ctx->trig + 2 * ctx->gnx;
+    a.cy_tab = ctx->trig + 2 * ctx->gnx + ctx->cfg.ny;
   }
   a.newton_iters = ctx->newton;
   a.step_dev = reinterpret_cast<long long*>(ctx->dscal + 6);
@@ -328,6 +388,9 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.lam_valid = ctx->lam_valid ? 1 : 0;
   a.peer_fence = ctx->peer ? 1 : 0;
   if (ctx->peer) a.fused_finalize = 0;
+  a.xghost = ctx->xg ? 1 : 0;
+  a.col0 = ctx->col0;
+  a.gnx = ctx->gnx;
   return a;
 }
 
@@ -343,14 +406,9 @@ void dispatch(int system, Args&&... args) {
 
 template <class Sys, int D, bool XPER, bool ADAPT>
 void launch_pair_1(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
-  auto k = fv_step_pair_kernel<Sys, XPER, ADAPT, kWarps, D>;
+  // (the dynamic shared-memory opt-in was set once at fv2d_create: preload_kernels)
   const int smem = kWarps * D * Sys::NV * 64 * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  k<<<grid, kWarps * 32, smem, ctx->launch_stream>>>(a);
+  fv_step_pair_kernel<Sys, XPER, ADAPT, kWarps, D><<<grid, kWarps * 32, smem, ctx->launch_stream>>>(a);
 }
 
 template <class Sys, int D>
@@ -369,7 +427,7 @@ struct LaunchStep {
       fv_step_naive_kernel<Sys><<<grid, 256, 0, ctx->launch_stream>>>(a);
     } else {
       constexpr int D = 4;
-      const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC;
+      const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC && !ctx->xg;
       // spray (nVar 6) uses the one-cell kernel: its fused source needs the registers
       if constexpr (Sys::NV == 6) {
         const int cols = 30 * kWarps;
@@ -416,22 +474,120 @@ struct LaunchArgmax {
   }
 };
 
+// Load every kernel a context can launch, and set the pair kernels' dynamic
+// shared-memory opt-in, once per process and system at fv2d_create -- never
+// while stepping.  Both a lazy module load and cudaFuncSetAttribute can wait
+// for kernels already running in the same CUDA context; when several ranks of
+// the peer-memory path share one process, a rank's spinning collective kernel
+// would then hold back another rank's first step (a deadlock until the
+// collective's timeout).  cudaFuncGetAttributes forces the load.
+template <class F>
+cudaError_t touch(F* f) {
+  cudaFuncAttributes at;
+  return cudaFuncGetAttributes(&at, (const void*)f);
+}
+template <class Sys, int D>
+cudaError_t pair_attrs() {
+  const int smem = kWarps * D * Sys::NV * 64 * (int)sizeof(double);
+  cudaError_t e = cudaSuccess;
+  for (cudaError_t r : {cudaFuncSetAttribute(fv_step_pair_kernel<Sys, true, false, kWarps, D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                        cudaFuncSetAttribute(fv_step_pair_kernel<Sys, true, true, kWarps, D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                        cudaFuncSetAttribute(fv_step_pair_kernel<Sys, false, false, kWarps, D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                        cudaFuncSetAttribute(fv_step_pair_kernel<Sys, false, true, kWarps, D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem)})
+    if (e == cudaSuccess) e = r;
+  return e;
+}
+template <class Sys>
+struct Preload {
+  static cudaError_t run() {
+    cudaError_t e = cudaSuccess;
+    auto t = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+    t(pair_attrs<Sys, 4>());
+    t(pair_attrs<Sys, 6>());
+    t(pair_attrs<Sys, 8>());
+    t(touch(fv_step_naive_kernel<Sys>));
+    t(touch(reduce_smax_kernel<Sys>));
+    t(touch(argmax_kernel<Sys>));
+    t(touch(fv_step_kernel<Sys, true, false, kWarps, 4>));
+    t(touch(fv_step_kernel<Sys, true, true, kWarps, 4>));
+    t(touch(fv_step_kernel<Sys, false, false, kWarps, 4>));
+    t(touch(fv_step_kernel<Sys, false, true, kWarps, 4>));
+    t(touch(fv_step_pair_kernel<Sys, true, false, kWarps, 4>));
+    t(touch(fv_step_pair_kernel<Sys, true, true, kWarps, 4>));
+    t(touch(fv_step_pair_kernel<Sys, false, false, kWarps, 4>));
+    t(touch(fv_step_pair_kernel<Sys, false, true, kWarps, 4>));
+    t(touch(finalize_kernel));
+    t(touch(peer_collective_kernel));
+    t(touch(promote_pending_kernel));
+    t(touch(spray_source_kernel));
+    t(touch(spray_source_step_kernel));
+    t(touch(fill_halo_kernel));
+    t(touch(fill_halo_cols_kernel));
+    t(touch(unpack_col_kernel));
+    t(touch(aos_to_dev_kernel));
+    t(touch(dev_to_aos_kernel));
+    return e;
+  }
+};
+cudaError_t preload_kernels(int system, int device) {  // (the current device)
+  static std::mutex mu;
+  static std::set<std::pair<int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({device, system})) return cudaSuccess;
+  cudaError_t e;
+  switch (system) {
+    case FV2D_ADVECTION: e = Preload<Advection>::run(); break;
+    case FV2D_EULER: e = Preload<Euler>::run(); break;
+    default: e = Preload<Spray>::run(); break;
+  }
+  if (e == cudaSuccess) done.insert({device, system});
+  return e;
+}
+
 int cur_parity(const fv2d_ctx* ctx) { return (int)(ctx->steps & 1); }
 
 // NCCL halo exchange into ghost buffers of parity q, from send_s/send_n.
 fv2d_status exchange(fv2d_ctx* ctx, int q, cudaStream_t stream = nullptr) {
   if (!ctx->use_nccl) return FV2D_OK;
   if (!stream) stream = ctx->stream;
-  const int r = ctx->cfg.rank, P = ctx->cfg.nranks;
+  const int x = ctx->rx, y = ctx->ry, PY = ctx->py, PX = ctx->px;
   const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
-  const bool has_s = r > 0 || per, has_n = r < P - 1 || per;
-  const size_t cnt = (size_t)ctx->rs;  // one whole cell row: nv variable rows
+  const bool has_s = y > 0 || per, has_n = y < PY - 1 || per;
+  const int rs_ = rank_at(ctx, x, y - 1), rn_ = rank_at(ctx, x, y + 1);
+  const size_t cnt = (size_t)ctx->rs;  // one whole cell row: nv variable rows (ghost columns included)
+  // Per peer, NCCL matches sends and receives in posting order; posting
+  // "send to the lower side, receive from the upper side, send to the upper
+  // side, receive from the lower side" keeps that correct when both sides are
+  // the same peer (2 blocks along an axis).
   CKN(g_nccl.GroupStart());
-  if (has_s) CKN(g_nccl.Send(ctx->send_s, cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, stream));
-  if (has_n) CKN(g_nccl.Recv(ghost_n(ctx, 0, q), cnt, ncclFloat64, (r + 1) % P, ctx->comm, stream));
-  if (has_n) CKN(g_nccl.Send(ctx->send_n, cnt, ncclFloat64, (r + 1) % P, ctx->comm, stream));
-  if (has_s) CKN(g_nccl.Recv(ghost_s(ctx, 0, q), cnt, ncclFloat64, (r - 1 + P) % P, ctx->comm, stream));
+  if (has_s) CKN(g_nccl.Send(ctx->send_s, cnt, ncclFloat64, rs_, ctx->comm, stream));
+  if (has_n) CKN(g_nccl.Recv(ghost_n(ctx, 0, q) - ctx->xoff, cnt, ncclFloat64, rn_, ctx->comm, stream));
+  if (has_n) CKN(g_nccl.Send(ctx->send_n, cnt, ncclFloat64, rn_, ctx->comm, stream));
+  if (has_s) CKN(g_nccl.Recv(ghost_s(ctx, 0, q) - ctx->xoff, cnt, ncclFloat64, rs_, ctx->comm, stream));
+  const bool perx = ctx->cfg.bc_x == FV2D_BC_PERIODIC;
+  const bool has_w = ctx->xg && (x > 0 || perx), has_e = ctx->xg && (x < PX - 1 || perx);
+  const int rw_ = rank_at(ctx, x - 1, y), re_ = rank_at(ctx, x + 1, y);
+  const size_t cc = (size_t)ctx->nv * ctx->H;  // one packed column
+  if (has_w) CKN(g_nccl.Send(ctx->send_w, cc, ncclFloat64, rw_, ctx->comm, stream));
+  if (has_e) CKN(g_nccl.Recv(ctx->recv_e, cc, ncclFloat64, re_, ctx->comm, stream));
+  if (has_e) CKN(g_nccl.Send(ctx->send_e, cc, ncclFloat64, re_, ctx->comm, stream));
+  if (has_w) CKN(g_nccl.Recv(ctx->recv_w, cc, ncclFloat64, rw_, ctx->comm, stream));
   CKN(g_nccl.GroupEnd());
+  const int nb = (ctx->H + 127) / 128;
+  if (has_w) {
+    unpack_col_kernel<<<nb, 128, 0, stream>>>(ctx->recv_w, row_ptr(ctx, 0, q, 0) - 1, ctx->nv, ctx->H, ctx->pitch,
+                                               ctx->rs);
+    CKL();
+  }
+  if (has_e) {
+    unpack_col_kernel<<<nb, 128, 0, stream>>>(ctx->recv_e, row_ptr(ctx, 0, q, 0) + ctx->nx, ctx->nv, ctx->H,
+                                               ctx->pitch, ctx->rs);
+    CKL();
+  }
   return FV2D_OK;
 }
 
@@ -608,6 +764,8 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
       if (ctx->buf[s][p]) cudaFree(ctx->buf[s][p]);
   if (ctx->send_s) cudaFree(ctx->send_s);
   if (ctx->send_n) cudaFree(ctx->send_n);
+  for (double* b : {ctx->send_w, ctx->send_e, ctx->recv_w, ctx->recv_e})
+    if (b) cudaFree(b);
   if (ctx->staging) cudaFree(ctx->staging);
   if (ctx->dscal) cudaFree(ctx->dscal);
   if (ctx->done) cudaFree(ctx->done);
@@ -645,18 +803,25 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   const int nv = nvar_of(c.system);
   if (nv < 0 || c.nvar != nv || c.nx < 1 || c.ny < 1 || c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks ||
       c.nslabs < 1 || c.nslabs > kMaxSlabs || ((c.nranks > 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK)) && c.nslabs != 1) ||
-      c.ny % (c.nranks * c.nslabs) != 0 || !(c.x1 > c.x0) || !(c.y1 > c.y0) || c.bc_x < 0 || c.bc_x > 2 ||
+      c.ny % ((c.nranks_x > 1 ? c.nranks / c.nranks_x : c.nranks) * c.nslabs) != 0 || !(c.x1 > c.x0) || !(c.y1 > c.y0) || c.bc_x < 0 || c.bc_x > 2 ||
       c.bc_y < 0 || c.bc_y > 2)
     return FV2D_E_ARG;
   if (c.system == FV2D_ADVECTION && (c.bc_x == FV2D_BC_WALL || c.bc_y == FV2D_BC_WALL)) return FV2D_E_ARG;
   if (c.system == FV2D_EULER && !(c.param[0] > 1.0)) return FV2D_E_ARG;
   if (c.system == FV2D_SPRAY && !(c.param[1] > 0.0)) return FV2D_E_ARG;
-  for (int k = 0; k < 5; ++k)
+  for (int k = 0; k < 4; ++k)
     if (c.reserved[k] != 0) return FV2D_E_ARG;
+  // 2-D rank blocks (nranks_x > 1): nranks_x x (nranks/nranks_x) blocks
+  const int px = c.nranks_x <= 1 ? 1 : c.nranks_x;
+  const bool xg = px > 1 || (c.flags & FV2D_FLAG_GHOST_COLUMNS);
+  if (c.nranks_x < 0 || c.nranks % px != 0 || c.nx % px != 0 || c.nx / px < 2 || (px > 1 && c.nslabs != 1))
+    return FV2D_E_ARG;
+  const int py = c.nranks / px;
+  const int nxl = c.nx / px;
   if (c.tiles_x < 0 || c.tiles_y < 0 || c.tiles_x > 256 || c.tiles_y > 256) return FV2D_E_ARG;
-  const long long H = c.ny / (c.nranks * c.nslabs);
+  const long long H = c.ny / (py * c.nslabs);
   if (H < 1) return FV2D_E_ARG;
-  if (std::max(1, c.tiles_y) > H || 2 * std::max(1, c.tiles_x) > c.nx) return FV2D_E_ARG;
+  if (std::max(1, c.tiles_y) > H || 2 * std::max(1, c.tiles_x) > nxl) return FV2D_E_ARG;
   const bool peer = (c.flags & FV2D_FLAG_PEER_HALO) != 0;
   if (peer && (c.nranks < 2 || c.nranks > kMaxRanks || c.nslabs != 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK)))
     return FV2D_E_ARG;
@@ -672,14 +837,22 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   ctx->tiles_x = std::max(1, c.tiles_x);
   ctx->tiles_y = std::max(1, c.tiles_y);
   ctx->nv = nv;
-  ctx->nx = c.nx;
+  ctx->px = px;
+  ctx->py = py;
+  ctx->rx = c.rank % px;
+  ctx->ry = c.rank / px;
+  ctx->gnx = c.nx;
+  ctx->nx = nxl;
+  ctx->col0 = ctx->rx * nxl;
+  ctx->xg = xg;
+  ctx->xoff = xg ? 2 : 0;  // row: [pad, ghost -1 | 0 .. nx-1 | ghost nx, ...]
   ctx->H = (int)H;
-  ctx->pitch = (c.nx + 31) / 32 * 32;
+  ctx->pitch = (nxl + ctx->xoff + (xg ? 1 : 0) + 31) / 32 * 32;
   if (const char* e = getenv("FV2D_RING_DEPTH")) ctx->ring_depth = atoi(e);  // tuning knob
   ctx->rs = (long long)ctx->pitch * nv;
-  ctx->rps = pick_rps(c.nx, (int)H);
+  ctx->rps = pick_rps(nxl, (int)H);
   ctx->nslabs = c.nslabs;
-  ctx->G = c.nranks * c.nslabs;
+  ctx->G = py * c.nslabs;
   ctx->dx = (c.x1 - c.x0) / c.nx;
   ctx->dy = (c.y1 - c.y0) / c.ny;
   ctx->hmin = ctx->dx < ctx->dy ? ctx->dx : ctx->dy;
@@ -715,7 +888,15 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     CKC(cudaMalloc(&ctx->send_n, row_bytes));
     CKC(cudaMemset(ctx->send_s, 0, row_bytes));
     CKC(cudaMemset(ctx->send_n, 0, row_bytes));
+    if (xg) {
+      const size_t col_bytes = (size_t)nv * H * sizeof(double);
+      for (double** b : {&ctx->send_w, &ctx->send_e, &ctx->recv_w, &ctx->recv_e}) {
+        CKC(cudaMalloc(b, col_bytes));
+        CKC(cudaMemset(*b, 0, col_bytes));
+      }
+    }
   }
+  CKC(preload_kernels(c.system, c.device));
   if (peer) {
     CKC(cudaMalloc(&ctx->sync, sizeof(PeerSync)));
     CKC(cudaMemset(ctx->sync, 0, sizeof(PeerSync)));
@@ -751,17 +932,31 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   // Dirichlet ghost rows are constant for the whole run.
   if (c.bc_y == FV2D_BC_DIRICHLET) {
     for (int s = 0; s < ctx->nslabs; ++s) {
-      const int g = c.rank * c.nslabs + s;
+      const int g = ctx->ry * c.nslabs + s;
       for (int p = 0; p < 2; ++p) {
         if (g == 0)
-          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ghost_s(ctx, s, p), nv, c.nx, ctx->pitch, c.dirichlet[0],
-                                                             c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
-                                                             c.dirichlet[4], c.dirichlet[5]);
+          fill_const_row_kernel<<<(nxl + 255) / 256, 256>>>(ghost_s(ctx, s, p), nv, nxl, ctx->pitch, c.dirichlet[0],
+                                                            c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
+                                                            c.dirichlet[4], c.dirichlet[5]);
         if (g == ctx->G - 1)
-          fill_const_row_kernel<<<(c.nx + 255) / 256, 256>>>(ghost_n(ctx, s, p), nv, c.nx, ctx->pitch, c.dirichlet[0],
-                                                             c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
-                                                             c.dirichlet[4], c.dirichlet[5]);
+          fill_const_row_kernel<<<(nxl + 255) / 256, 256>>>(ghost_n(ctx, s, p), nv, nxl, ctx->pitch, c.dirichlet[0],
+                                                            c.dirichlet[1], c.dirichlet[2], c.dirichlet[3],
+                                                            c.dirichlet[4], c.dirichlet[5]);
       }
+    }
+    CKC(cudaGetLastError());
+  }
+  // ... and so are Dirichlet ghost columns of blocks on the global x boundary
+  if (xg && c.bc_x == FV2D_BC_DIRICHLET) {
+    for (int s = 0; s < ctx->nslabs; ++s)
+    for (int p = 0; p < 2; ++p) {
+      double* cols[2] = {ctx->rx == 0 ? ghost_s(ctx, s, p) - 1 : nullptr,
+                         ctx->rx == px - 1 ? ghost_s(ctx, s, p) + nxl : nullptr};
+      for (double* col : cols)
+        if (col)
+          fill_const_col_kernel<<<(int)((H + 2 + 127) / 128), 128>>>(col, nv, (int)H + 2, ctx->pitch, ctx->rs,
+                                                                     c.dirichlet[0], c.dirichlet[1], c.dirichlet[2],
+                                                                     c.dirichlet[3], c.dirichlet[4], c.dirichlet[5]);
     }
     CKC(cudaGetLastError());
   }
@@ -783,6 +978,10 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   for (int s = 0; s < ctx->nslabs; ++s) a.slab[s].in = row_ptr(ctx, s, 0, 0);
   fill_halo_kernel<<<dim3((ctx->nx + 127) / 128, 1, ctx->nslabs), 128, 0, ctx->stream>>>(a, ctx->nv);
   CKL();
+  if (ctx->xg) {
+    fill_halo_cols_kernel<<<dim3((ctx->H + 127) / 128, 1, ctx->nslabs), 128, 0, ctx->stream>>>(a, ctx->nv);
+    CKL();
+  }
   fv2d_status st = exchange(ctx, 0);
   if (st) return st;
   unsigned long long init[8] = {0, 0, 0, ~0ull, 0, 0, 0, 0};
@@ -989,7 +1188,7 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
   // exchange on the comm stream overlapped with the interior strips.
   const int hb = 8;
   const bool overlap =
-      ctx->use_nccl && !split && !tiled && !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H > 4 * hb;
+      ctx->use_nccl && !split && !tiled && !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H > 4 * hb && !ctx->xg;
   if (overlap) {
     StepArgs ab = at, ai = at;
     set_ranges(ab, 0, hb, hb, ctx->H - hb, ctx->H, hb);
@@ -1292,6 +1491,17 @@ fv2d_status fv2d_host_free(void* ptr) {
   return cudaFreeHost(ptr) == cudaSuccess ? FV2D_OK : FV2D_E_CUDA;
 }
 
+// Ranks of the south, north, west, east neighbour blocks (-1: none, i.e. a
+// non-periodic global boundary; W/E only for 2-D rank blocks).
+static void peer_neighbours(const fv2d_ctx* ctx, int nb[4]) {
+  const bool pery = ctx->cfg.bc_y == FV2D_BC_PERIODIC, perx = ctx->cfg.bc_x == FV2D_BC_PERIODIC;
+  const int x = ctx->rx, y = ctx->ry;
+  nb[0] = (y > 0 || pery) ? rank_at(ctx, x, y - 1) : -1;
+  nb[1] = (y < ctx->py - 1 || pery) ? rank_at(ctx, x, y + 1) : -1;
+  nb[2] = ctx->xg && (x > 0 || perx) ? rank_at(ctx, x - 1, y) : -1;
+  nb[3] = ctx->xg && (x < ctx->px - 1 || perx) ? rank_at(ctx, x + 1, y) : -1;
+}
+
 static fv2d_status peer_finish(fv2d_ctx* ctx) {
   ctx->pa.nranks = ctx->cfg.nranks;
   ctx->pa.me = ctx->cfg.rank;
@@ -1316,52 +1526,54 @@ fv2d_status fv2d_peer_connect(fv2d_ctx* ctx, const uint8_t* all) {
   if (!ctx || !all || !ctx->peer) return FV2D_E_ARG;
   CK(cudaSetDevice(ctx->cfg.device));
   const int P = ctx->cfg.nranks, r = ctx->cfg.rank;
-  const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
-  auto open = [&](int rank, int k, void** ptr) -> fv2d_status {
-    cudaIpcMemHandle_t h;
-    memcpy(&h, all + (size_t)rank * FV2D_PEER_HANDLE_BYTES + (size_t)k * 64, 64);
-    CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
-    ctx->ipc_opened.push_back(*ptr);
+  // every handle opened at most once (a rank can be several neighbours);
+  // this rank's own buffers are used directly
+  std::vector<void*> opened((size_t)P * 3, nullptr);
+  auto get = [&](int rank, int k, void** ptr) -> fv2d_status {
+    if (rank == r) {
+      *ptr = k == 2 ? (void*)ctx->sync : (void*)ctx->buf[0][k];
+      return FV2D_OK;
+    }
+    void*& slot = opened[(size_t)rank * 3 + k];
+    if (!slot) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, all + (size_t)rank * FV2D_PEER_HANDLE_BYTES + (size_t)k * 64, 64);
+      CK(cudaIpcOpenMemHandle(&slot, h, cudaIpcMemLazyEnablePeerAccess));
+      ctx->ipc_opened.push_back(slot);
+    }
+    *ptr = slot;
     return FV2D_OK;
   };
   for (int q = 0; q < P; ++q) {
     if (q == r) continue;
     void* p = nullptr;
-    fv2d_status st = open(q, 2, &p);
+    fv2d_status st = get(q, 2, &p);
     if (st) return st;
     ctx->pa.sync[q] = (PeerSync*)p;
   }
-  const int s_rank = (r > 0 || per) ? (r - 1 + P) % P : -1;
-  const int n_rank = (r < P - 1 || per) ? (r + 1) % P : -1;
-  void* bs[2] = {nullptr, nullptr};
-  void* bn[2] = {nullptr, nullptr};
-  for (int k = 0; k < 2; ++k) {
-    if (s_rank >= 0) {
-      fv2d_status st = open(s_rank, k, &bs[k]);
-      if (st) return st;
-    }
-    if (n_rank >= 0) {
-      if (n_rank == s_rank) bn[k] = bs[k];
-      else {
-        fv2d_status st = open(n_rank, k, &bn[k]);
+  int nb[4];
+  peer_neighbours(ctx, nb);
+  double** tgt[4] = {ctx->peer_buf_s, ctx->peer_buf_n, ctx->peer_buf_w, ctx->peer_buf_e};
+  for (int d = 0; d < 4; ++d)
+    for (int k = 0; k < 2; ++k) {
+      void* p = nullptr;
+      if (nb[d] >= 0) {
+        fv2d_status st = get(nb[d], k, &p);
         if (st) return st;
       }
+      tgt[d][k] = (double*)p;
     }
-  }
-  for (int k = 0; k < 2; ++k) {
-    ctx->peer_buf_s[k] = (double*)bs[k];
-    ctx->peer_buf_n[k] = (double*)bn[k];
-  }
   return peer_finish(ctx);
 }
 
 fv2d_status fv2d_peer_connect_local(fv2d_ctx* ctx, fv2d_ctx* const* group) {
   if (!ctx || !group || !ctx->peer) return FV2D_E_ARG;
   CK(cudaSetDevice(ctx->cfg.device));
-  const int P = ctx->cfg.nranks, r = ctx->cfg.rank;
-  const bool per = ctx->cfg.bc_y == FV2D_BC_PERIODIC;
+  const int P = ctx->cfg.nranks;
   for (int q = 0; q < P; ++q) {
-    if (!group[q] || group[q]->cfg.rank != q || group[q]->cfg.nranks != P || !group[q]->peer) return FV2D_E_ARG;
+    if (!group[q] || group[q]->cfg.rank != q || group[q]->cfg.nranks != P || !group[q]->peer ||
+        group[q]->px != ctx->px || group[q]->xg != ctx->xg)
+      return FV2D_E_ARG;
     if (group[q]->cfg.device != ctx->cfg.device) {
       cudaError_t e = cudaDeviceEnablePeerAccess(group[q]->cfg.device, 0);
       if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
@@ -1371,12 +1583,11 @@ fv2d_status fv2d_peer_connect_local(fv2d_ctx* ctx, fv2d_ctx* const* group) {
     }
     ctx->pa.sync[q] = group[q]->sync;
   }
-  const int s_rank = (r > 0 || per) ? (r - 1 + P) % P : -1;
-  const int n_rank = (r < P - 1 || per) ? (r + 1) % P : -1;
-  for (int k = 0; k < 2; ++k) {
-    ctx->peer_buf_s[k] = s_rank >= 0 ? group[s_rank]->buf[0][k] : nullptr;
-    ctx->peer_buf_n[k] = n_rank >= 0 ? group[n_rank]->buf[0][k] : nullptr;
-  }
+  int nb[4];
+  peer_neighbours(ctx, nb);
+  double** tgt[4] = {ctx->peer_buf_s, ctx->peer_buf_n, ctx->peer_buf_w, ctx->peer_buf_e};
+  for (int d = 0; d < 4; ++d)
+    for (int k = 0; k < 2; ++k) tgt[d][k] = nb[d] >= 0 ? group[nb[d]]->buf[0][k] : nullptr;
   return peer_finish(ctx);
 }
 

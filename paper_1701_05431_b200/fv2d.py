@@ -20,6 +20,7 @@ BC_PERIODIC, BC_DIRICHLET, BC_WALL = 0, 1, 2
 AOS, SOA = 0, 1
 FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL, FLAG_NCCL_LOOPBACK, FLAG_FUSE_SOURCE, FLAG_GRAPH, FLAG_PEER_HALO = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
+FLAG_GHOST_COLUMNS = 0x80
 PEER_HANDLE_BYTES = 192
 NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
 _NAMES = {OK: "OK", E_ARG: "E_ARG", E_CFL: "E_CFL", E_NONFINITE: "E_NONFINITE", E_RECON: "E_RECON",
@@ -33,7 +34,7 @@ class Config(C.Structure):
                 ("param", C.c_double * 8), ("dirichlet", C.c_double * 6),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("nslabs", C.c_int32), ("device", C.c_int32),
                 ("flags", C.c_uint32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
-                ("reserved", C.c_int32 * 5)]
+                ("nranks_x", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 class Stats(C.Structure):
@@ -155,7 +156,7 @@ class Solver:
 
     def __init__(self, nx, ny, system=EULER, *, x0=0.0, x1=1.0, y0=0.0, y1=1.0, param=None,
                  bc_x=BC_PERIODIC, bc_y=BC_PERIODIC, dirichlet=(), rank=0, nranks=1, nslabs=1, device=0,
-                 flags=0, tiles=(1, 1), nccl_id: bytes | None = None, stream: int | None = None):
+                 flags=0, tiles=(1, 1), nranks_x=1, nccl_id: bytes | None = None, stream: int | None = None):
         L = lib()
         cfg = Config()
         rc = L.fv2d_config_default(C.byref(cfg), nx, ny, system)
@@ -172,9 +173,12 @@ class Solver:
         cfg.bc_x, cfg.bc_y = bc_x, bc_y
         cfg.rank, cfg.nranks, cfg.nslabs, cfg.device, cfg.flags = rank, nranks, nslabs, device, flags
         cfg.tiles_x, cfg.tiles_y = tiles
+        cfg.nranks_x = nranks_x
         self.cfg = cfg
         self.nx, self.ny, self.nv, self.system = nx, ny, NVAR[system], system
-        self.ny_local = ny // nranks
+        px = max(1, nranks_x)
+        self.ny_local = ny // (nranks // px)  # this rank's block (fv2d.h: Layouts)
+        self.nx_local = nx // px
         if nranks > 1 or (flags & FLAG_NCCL_LOOPBACK):
             _preload_nccl()
         h = C.c_void_p()
@@ -216,7 +220,7 @@ class Solver:
 
     # -- state
     def _shape(self, layout):
-        return (self.ny_local, self.nx, self.nv) if layout == AOS else (self.nv, self.ny_local, self.nx)
+        return (self.ny_local, self.nx_local, self.nv) if layout == AOS else (self.nv, self.ny_local, self.nx_local)
 
     def set_state(self, W: np.ndarray, layout: int = AOS):
         W = np.ascontiguousarray(W, dtype=np.float64)

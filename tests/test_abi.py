@@ -63,6 +63,28 @@ def test_create_validates_before_touching_the_device():
     assert L.fv2d_destroy(None) == fv2d.OK
 
 
+def test_create_validates_2d_rank_blocks():
+    """nranks_x (2-D blocks): nranks % nranks_x == 0, nx % nranks_x == 0, blocks
+    at least 2 columns wide, ny divisible by the block rows, one slab per rank."""
+    L = fv2d.lib()
+    h = C.c_void_p()
+    cfg = fv2d.Config()
+    for (nx, ny, nranks, px, nslabs) in [(64, 32, 4, 3, 1),   # 4 % 3
+                                         (66, 32, 4, 4, 1),   # 66 % 4
+                                         (6, 32, 4, 4, 1),    # 6 % 4 (and < 2 columns)
+                                         (4, 32, 4, 4, 1),    # 1-column blocks
+                                         (64, 30, 8, 2, 1),   # 30 % (8/2)
+                                         (64, 32, 4, 2, 2),   # slabs with blocks
+                                         (64, 32, 4, -1, 1)]:
+        L.fv2d_config_default(C.byref(cfg), nx, ny, fv2d.EULER)
+        cfg.nranks, cfg.nranks_x, cfg.nslabs = nranks, px, nslabs
+        cfg.flags = fv2d.FLAG_PEER_HALO
+        assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG, (nx, ny, nranks, px, nslabs)
+    L.fv2d_config_default(C.byref(cfg), 64, 32, fv2d.EULER)
+    cfg.reserved[0] = 1                 # reserved words must be 0
+    assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
+
+
 def test_c_client_compiles_against_the_header():
     """The ABI is usable from plain C (examples/c_client.c): header + .so only."""
     exe = os.path.join(ROOT, "examples", "c_client")

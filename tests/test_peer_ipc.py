@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, bc_y, nsteps, q):
+def _rank(rank, world, port, bc_y, nsteps, q, px=1):
     import torch
     import torch.distributed as dist
 
@@ -34,15 +34,16 @@ def _rank(rank, world, port, bc_y, nsteps, q):
     try:
         nx, ny = 140, 64
         W0 = inputs.euler_random(nx, ny, seed=77)
-        H = ny // world
+        H, Wd = ny // (world // px), nx // px
+        rx, ry = rank % px, rank // px
         st = torch.cuda.Stream()
-        s = fv2d.Solver(nx, ny, fv2d.EULER, param=(1.4,), bc_y=bc_y, rank=rank, nranks=world,
+        s = fv2d.Solver(nx, ny, fv2d.EULER, param=(1.4,), bc_y=bc_y, rank=rank, nranks=world, nranks_x=px,
                         flags=fv2d.FLAG_PEER_HALO, stream=st.cuda_stream)
         handles = [None] * world
         dist.all_gather_object(handles, s.peer_export())
         s.peer_connect(b"".join(handles))
         dist.barrier()
-        s.set_state(W0[rank * H:(rank + 1) * H])
+        s.set_state(W0[ry * H:(ry + 1) * H, rx * Wd:(rx + 1) * Wd])
         log = s.step_adaptive(0.45, nsteps)
         W = s.get_state()
         out = [None] * world
@@ -55,13 +56,14 @@ def _rank(rank, world, port, bc_y, nsteps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("bc_y", [O.BC_PERIODIC, O.BC_WALL])
-def test_peer_ipc_two_processes_bitwise(bc_y):
+@pytest.mark.parametrize("bc_y,px", [(O.BC_PERIODIC, 1), (O.BC_WALL, 1), (O.BC_WALL, 2)])
+def test_peer_ipc_two_processes_bitwise(bc_y, px):
+    """px = 1: two y-slabs; px = 2: two x-blocks (east/west ghost columns over IPC)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
     nsteps = 15
-    ps = [ctx.Process(target=_rank, args=(r, 2, port, bc_y, nsteps, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rank, args=(r, 2, port, bc_y, nsteps, q, px)) for r in range(2)]
     for p in ps:
         p.start()
     out = q.get(timeout=600)
@@ -70,7 +72,7 @@ def test_peer_ipc_two_processes_bitwise(bc_y):
         assert p.exitcode == 0
     cfg = O.Config(nx=140, ny=64, system=O.EULER, param=(1.4,), bc_y=bc_y)
     ref = O.run(cfg, inputs.euler_random(140, 64, seed=77), nsteps, O.ADAPTIVE, 0.45)
-    W = np.concatenate([o[0] for o in out], axis=0)
+    W = np.concatenate([o[0] for o in out], axis=1 if px == 2 else 0)
     for o in out:
         assert np.array_equal(o[1], ref.dt_log)
     assert np.array_equal(W, ref.W)
