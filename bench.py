@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--peer-halo", action="store_true",
                     help="N>1: halo rows and the CFL all-reduce through peer memory (CUDA IPC) instead of NCCL")
     ap.add_argument("--adaptive", action="store_true", help="adaptive dt (smax reduced in the epilogue)")
+    ap.add_argument("--nranks-x", type=int, default=1,
+                    help="N>1: the ranks as a PX x (N/PX) grid of 2-D blocks (E/W ghost columns) instead of y-slabs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -225,9 +227,10 @@ def main():
     system, nx, ny_global, desc = WORKLOADS[args.workload]
     weak = args.workload.startswith("c5")
     ny = ny_global * world if weak else ny_global
-    if ny % world:
-        raise SystemExit(f"ny={ny} not divisible by {world}")
-    j0, j1 = D.slab_rows(rank, world, ny)
+    px = max(1, args.nranks_x)
+    if world % px or ny % (world // px) or nx % px:
+        raise SystemExit(f"{nx}x{ny} cells do not split into {px}x{world // px} blocks")
+    j0, j1, i0, i1 = D.block_of(rank, px, world // px, nx, ny)
     H = j1 - j0
     nccl_id = None
     peer = world > 1 and args.peer_halo
@@ -237,12 +240,14 @@ def main():
     flags = (fv2d.FLAG_NAIVE if args.naive else 0) | (fv2d.FLAG_ONE_CELL if args.one_cell else 0) | \
         (fv2d.FLAG_PEER_HALO if peer else 0)
     s = fv2d.Solver(nx, ny, fv2d.EULER, param=(GAMMA,), rank=rank, nranks=world, device=local, flags=flags,
-                    nccl_id=nccl_id, stream=stream.cuda_stream)
+                    nranks_x=px, nccl_id=nccl_id, stream=stream.cuda_stream)
     if peer:
         handles = [None] * world
         dist.all_gather_object(handles, s.peer_export())
         s.peer_connect(b"".join(handles))
     W0 = gen_ic(system, nx, ny, (j0, j1))
+    if px > 1:
+        W0 = np.ascontiguousarray(W0[:, i0:i1])
     s.set_state(W0)
     dt, smax0 = s.compute_dt(CFL)    # the paper's constant dt, set at start
 
@@ -312,7 +317,7 @@ def main():
     if rank == 0:
         peak, peak_src = measured_peaks()
         bpc = BYTES_PER_CELL[system]
-        cells_per_launch = nx * H
+        cells_per_launch = (i1 - i0) * H
         achieved = bpc * cells_per_launch / (kern_max * 1e-3) / 1e9
         kernel = ("fv_step_naive_kernel<Euler>" if args.naive else
                   "fv_step_kernel<Euler> (one cell/lane)" if args.one_cell else "fv_step_pair_kernel<Euler>")
@@ -323,12 +328,13 @@ def main():
             "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.workload, "description": desc, "nx": nx, "ny": ny,
-                       "rows_per_gpu": H, "mode": "adaptive dt" if args.adaptive else "fixed dt (checked)",
+                       "rows_per_gpu": H, "cols_per_gpu": i1 - i0,
+                       "mode": "adaptive dt" if args.adaptive else "fixed dt (checked)",
                        "dt": dt, "kernel": kernel,
-                       "parallelism": f"y-slabs x{world}" + (
+                       "parallelism": (f"y-slabs x{world}" if px == 1 else f"2-D blocks {px}x{world // px}") + (
                            (" (peer-memory halo + all-reduce)" if peer else " (NCCL halo overlapped + all-reduce)")
                            if world > 1 else ""),
-                       "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % (nx * H * 32 / 1e9)},
+                       "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % ((i1 - i0) * H * 32 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_cell": bpc, "kernel_ms": kern_max, "cells_per_launch": cells_per_launch},
