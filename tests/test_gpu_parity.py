@@ -574,3 +574,27 @@ def test_c4_full_size_4096_spray_sampled_rows():
         band, _ = O.source_step(bcfg, band, dt)
         got = W1[[r % n for r in range(j0, j0 + 6)]]
         assert relerr(got, band[1:-1]) <= 1e-12
+
+
+@pytest.mark.parametrize("p0", [1.0, 1e-7])
+def test_adaptive_smax_near_ties_and_high_mach(p0):
+    """The adaptive epilogue skips cells that provably cannot raise the running
+    smax (Euler.below).  Adversarial input: a uniform state whose
+    cells differ only in the last bits (near-ties everywhere), at low and at
+    extreme Mach number (p = 1e-7: cancellation in p = gm1 (E - ke)).  The dt
+    sequence must still equal the oracle's exactly."""
+    nx, ny = 256, 128
+    rng = np.random.default_rng(11)
+    rho, u, v = 1.0, 0.3, -0.2
+    E = p0 / (G - 1) + 0.5 * rho * (u * u + v * v)
+    W0 = np.empty((ny, nx, 4))
+    W0[..., 0] = rho * (1 + rng.integers(-4, 5, (ny, nx)) * 2.0 ** -52)
+    W0[..., 1] = rho * u * (1 + rng.integers(-4, 5, (ny, nx)) * 2.0 ** -52)
+    W0[..., 2] = rho * v * (1 + rng.integers(-4, 5, (ny, nx)) * 2.0 ** -52)
+    W0[..., 3] = E * (1 + rng.integers(-4, 5, (ny, nx)) * 2.0 ** -52)
+    cfg = O.Config(nx=nx, ny=ny, system=O.EULER, param=(G,), x1=2.0)
+    ref = O.run(cfg, W0, 6, O.ADAPTIVE, 0.45)
+    for flags in (0, fv2d.FLAG_ONE_CELL):
+        W, log = gpu_run(cfg, W0, 6, O.ADAPTIVE, 0.45, flags=flags)
+        assert np.array_equal(log, ref.dt_log)
+        assert np.array_equal(W, ref.W)
