@@ -506,9 +506,11 @@ struct Preload {
   static cudaError_t run() {
     cudaError_t e = cudaSuccess;
     auto t = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
-    t(pair_attrs<Sys, 4>());
-    t(pair_attrs<Sys, 6>());
-    t(pair_attrs<Sys, 8>());
+    if constexpr (Sys::NV != 6) {  // spray transport always uses the one-cell kernel
+      t(pair_attrs<Sys, 4>());
+      t(pair_attrs<Sys, 6>());
+      t(pair_attrs<Sys, 8>());
+    }
     t(touch(fv_step_naive_kernel<Sys>));
     t(touch(reduce_smax_kernel<Sys>));
     t(touch(argmax_kernel<Sys>));
@@ -516,10 +518,6 @@ struct Preload {
     t(touch(fv_step_kernel<Sys, true, true, kWarps, 4>));
     t(touch(fv_step_kernel<Sys, false, false, kWarps, 4>));
     t(touch(fv_step_kernel<Sys, false, true, kWarps, 4>));
-    t(touch(fv_step_pair_kernel<Sys, true, false, kWarps, 4>));
-    t(touch(fv_step_pair_kernel<Sys, true, true, kWarps, 4>));
-    t(touch(fv_step_pair_kernel<Sys, false, false, kWarps, 4>));
-    t(touch(fv_step_pair_kernel<Sys, false, true, kWarps, 4>));
     t(touch(finalize_kernel));
     t(touch(peer_collective_kernel));
     t(touch(promote_pending_kernel));
