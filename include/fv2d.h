@@ -223,6 +223,22 @@ fv2d_status fv2d_last_error(fv2d_ctx* ctx, char* buf, size_t n, int64_t* step, i
  * into step_kernel_ms. */
 fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out);
 
+/* Host-resident stepping: W^0 = host_in (as fv2d_set_state), nsteps steps of
+ * the constant dt checked every step (as fv2d_step), host_out = the result (as
+ * fv2d_get_state); synchronous.  Same bits as those three calls.  For a
+ * single-rank, single-slab transport-only context (advection, Euler; y-slab
+ * layout) with layout FV2D_AOS the first step is pipelined over row bands:
+ * band b is copied host->device and converted while band b-1 is stepped and
+ * band b-2 is converted back and copied device->host, so the two copy
+ * directions and the kernels overlap (the bands next to the periodic/wall
+ * y-boundary are stepped last, after the ghost rows are filled).  Other
+ * contexts run the three calls in sequence.  host_out may equal host_in.
+ * Use fv2d_host_alloc (pinned) memory for overlapped copies.  On a latched
+ * error the state, and host_out, hold W^k of the failing step k (the output
+ * bands already copied are overwritten with W^k). */
+fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_out, fv2d_layout layout, double dt,
+                           int32_t nsteps);
+
 /* Asynchronous output (the paper's gatherForOutput -> switch -> outputToDisk
  * pipeline, which writes a snapshot without a global barrier):
  * enqueue a copy of the current state W^k of this rank's slab into `host`

@@ -154,6 +154,10 @@ struct fv2d_ctx {
   double* recv_e = nullptr;
   double* staging = nullptr;
   size_t staging_bytes = 0;
+  // fv2d_step_host pipeline: output staging, copy streams, per-band events
+  double* staging_out = nullptr;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  std::vector<cudaEvent_t> ev_band;
   // device scalars
   unsigned long long* dscal = nullptr;  // [0]=smax [1]=pending [2]=status [3]=bad_cell [4..5]=reduced
   unsigned int* done = nullptr;
@@ -322,7 +326,8 @@ int pick_rps(int ncols, int nrows) {
   const long long colblocks = ((ncols + 62) / 62 + kWarps - 1) / kWarps;
   static const int rps_force = getenv("FV2D_RPS") ? atoi(getenv("FV2D_RPS")) : 0;  // tuning knob
   if (rps_force > 0) return std::min(rps_force, std::max(1, nrows));
-  const long long rps = colblocks * nrows / (148 * 6);
+  static const int waves = getenv("FV2D_RPS_WAVES") ? atoi(getenv("FV2D_RPS_WAVES")) : 2;  // tuning knob
+  const long long rps = colblocks * nrows / (148 * 3 * std::max(1, waves));
   return (int)std::max<long long>(4, std::min<long long>(rps_max, rps));
 }
 
@@ -765,6 +770,10 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   for (double* b : {ctx->send_w, ctx->send_e, ctx->recv_w, ctx->recv_e})
     if (b) cudaFree(b);
   if (ctx->staging) cudaFree(ctx->staging);
+  if (ctx->staging_out) cudaFree(ctx->staging_out);
+  for (cudaEvent_t e : ctx->ev_band) cudaEventDestroy(e);
+  if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   if (ctx->dscal) cudaFree(ctx->dscal);
   if (ctx->done) cudaFree(ctx->done);
   if (ctx->dt_dev) cudaFree(ctx->dt_dev);
@@ -1350,6 +1359,144 @@ fv2d_status fv2d_step_adaptive(fv2d_ctx* ctx, double cfl, int32_t nsteps, double
     if (s) return report(ctx, s);
   }
   return FV2D_OK;
+}
+
+// Pipelined first step of fv2d_step_host (see fv2d.h).  Bands of R rows; band
+// b's AoS rows are contiguous in host memory and in the staging buffers.
+static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, double* host_out, double dt) {
+  const int nv = ctx->nv, nx = ctx->nx, H = ctx->H;
+  static const int nb = getenv("FV2D_HOST_BANDS") ? atoi(getenv("FV2D_HOST_BANDS")) : 64;  // tuning knob
+  const int R = std::max(64, (H + nb - 1) / std::max(1, nb));
+  const int B = (H + R - 1) / R;
+  const size_t row_doubles = (size_t)nx * nv;
+  const size_t bytes = row_doubles * H * sizeof(double);
+  if (ctx->snap_parity >= 0) {
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_snap_conv, 0));
+    ctx->snap_parity = -1;
+  }
+  fv2d_status st = ensure_staging(ctx);
+  if (st) return st;
+  if (!ctx->staging_out) CK(cudaMalloc(&ctx->staging_out, bytes));
+  if (!ctx->h2d_stream) CK(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+  if (!ctx->d2h_stream) CK(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+  while ((int)ctx->ev_band.size() < 3 * B + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ev_band.push_back(e);
+  }
+  cudaEvent_t* ev_in = ctx->ev_band.data();          // band b uploaded
+  cudaEvent_t* ev_conv = ev_in + B;                  // band b converted into the state buffer
+  cudaEvent_t* ev_out = ev_in + 2 * B;               // band b's W^{n+1} converted to AoS
+  cudaEvent_t ev_start = ctx->ev_band[3 * B];
+  auto lo = [&](int b) { return b * R; };
+  auto hi = [&](int b) { return std::min(H, (b + 1) * R); };
+  // W^0 -> parity 0, uploads in band order on the H2D stream (after prior work)
+  ctx->steps = 0;
+  CK(cudaEventRecord(ev_start, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->h2d_stream, ev_start, 0));
+  for (int b = 0; b < B; ++b) {
+    CK(cudaMemcpyAsync(ctx->staging + row_doubles * lo(b), host_in + row_doubles * lo(b),
+                       row_doubles * (hi(b) - lo(b)) * sizeof(double), cudaMemcpyHostToDevice, ctx->h2d_stream));
+    CK(cudaEventRecord(ev_in[b], ctx->h2d_stream));
+  }
+  // reset the step's device scalars as after_set_state does
+  unsigned long long init[8] = {0, 0, 0, ~0ull, 0, 0, 0, 0};
+  CK(cudaMemcpyAsync(ctx->dscal, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->done, 0, sizeof(unsigned int), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dt_dev, 0, sizeof(double), ctx->stream));
+  StepArgs a = make_args(ctx, 0);
+  a.adaptive = 0;
+  a.dt = dt;
+  a.step = 0;
+  a.fused_finalize = 0;
+  StepArgs hf = make_args(ctx, 1);  // halo targets of parity 0 (as after_set_state)
+  hf.slab[0].in = row_ptr(ctx, 0, 0, 0);
+  auto convert_in = [&](int b) -> fv2d_status {
+    CK(cudaStreamWaitEvent(ctx->stream, ev_in[b], 0));
+    aos_to_dev_kernel<<<148 * 2, 256, 0, ctx->stream>>>(ctx->staging + row_doubles * lo(b), row_ptr(ctx, 0, 0, lo(b)),
+                                                        nv, nx, hi(b) - lo(b), ctx->pitch, ctx->rs);
+    CKL();
+    CK(cudaEventRecord(ev_conv[b], ctx->stream));
+    return FV2D_OK;
+  };
+  auto step_band = [&](int b) -> fv2d_status {
+    StepArgs t = a;
+    set_ranges(t, lo(b), hi(b), pick_rps(nx, hi(b) - lo(b)), 0, 0, 1);
+    dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, t);
+    CKL();
+    dev_to_aos_kernel<<<148 * 2, 256, 0, ctx->stream>>>(row_ptr(ctx, 0, 1, lo(b)), ctx->staging_out + row_doubles * lo(b),
+                                                        nv, nx, hi(b) - lo(b), ctx->pitch, ctx->rs);
+    CKL();
+    CK(cudaEventRecord(ev_out[b], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->d2h_stream, ev_out[b], 0));
+    CK(cudaMemcpyAsync(host_out + row_doubles * lo(b), ctx->staging_out + row_doubles * lo(b),
+                       row_doubles * (hi(b) - lo(b)) * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    return FV2D_OK;
+  };
+  // interior bands as soon as their neighbours are resident; the boundary
+  // bands (0 and B-1, which read the ghost rows) after the halo fill
+  for (int b = 0; b < B; ++b) {
+    st = convert_in(b);
+    if (st) return st;
+    if (b >= 2 && b - 1 < B - 1) {
+      st = step_band(b - 1);
+      if (st) return st;
+    }
+  }
+  fill_halo_kernel<<<dim3((nx + 127) / 128, 1, 1), 128, 0, ctx->stream>>>(hf, nv);
+  CKL();
+  if (B > 1) {
+    st = step_band(B - 1);
+    if (st) return st;
+  }
+  st = step_band(0);
+  if (st) return st;
+  finalize_kernel<<<1, 32, 0, ctx->stream>>>(a, nullptr);
+  CKL();
+  CK(cudaEventRecord(ev_start, ctx->d2h_stream));
+  CK(cudaStreamWaitEvent(ctx->stream, ev_start, 0));
+  ctx->has_state = true;
+  ctx->dt_valid = false;
+  ctx->lam_valid = false;
+  ctx->err.clear();
+  ctx->err_step = ctx->err_cell = -1;
+  ctx->steps = 1;
+  return FV2D_OK;
+}
+
+fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_out, fv2d_layout layout, double dt,
+                           int32_t nsteps) {
+  if (!ctx || !host_in || !host_out || (layout != FV2D_AOS && layout != FV2D_SOA) || !(dt > 0.0) || nsteps < 0 ||
+      !std::isfinite(dt))
+    return FV2D_E_ARG;
+  if (ctx->peer && !ctx->peer_connected) return set_err(ctx, FV2D_E_STATE, "peer halo: call fv2d_peer_connect first");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const bool pipelined = layout == FV2D_AOS && nsteps >= 1 && ctx->cfg.nranks == 1 && ctx->nslabs == 1 &&
+                         !ctx->xg && !ctx->use_nccl && !ctx->peer && ctx->cfg.system != FV2D_SPRAY &&
+                         !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H >= 128;
+  fv2d_status st;
+  if (pipelined) {
+    st = ensure_dt_log(ctx, nsteps);
+    if (st) return st;
+    st = step_host_pipelined(ctx, host_in, host_out, dt);
+    if (st) return st;
+    if (nsteps > 1) {
+      st = launch_steps(ctx, 0, dt, 0.0, nsteps - 1);
+      if (st) return st;
+    } else {
+      unsigned long long s0;
+      st = read_status(ctx, &s0);  // also waits for the last D2H band
+      if (st) return st;
+      if (s0 == 0) return FV2D_OK;
+      // the step failed: host_out must hold W^0 (the already copied bands hold W^1)
+    }
+  } else {
+    st = fv2d_set_state(ctx, host_in, layout);
+    if (st) return st;
+    st = launch_steps(ctx, 0, dt, 0.0, nsteps);
+    if (st) return st;
+  }
+  return fv2d_get_state(ctx, host_out, layout);
 }
 
 fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {

@@ -79,12 +79,14 @@ def lib():
         L.fv2d_peer_export.argtypes = [vp, C.c_char_p]
         L.fv2d_peer_connect.argtypes = [vp, C.c_char_p]
         L.fv2d_peer_connect_local.argtypes = [vp, P(vp)]
+        L.fv2d_step_host.argtypes = [vp, vp, vp, C.c_int, C.c_double, C.c_int32]
         for name in ("fv2d_version", "fv2d_config_default", "fv2d_nccl_unique_id", "fv2d_create", "fv2d_destroy",
                      "fv2d_set_state", "fv2d_set_state_device", "fv2d_get_state", "fv2d_compute_dt",
                      "fv2d_check_dt", "fv2d_step", "fv2d_step_adaptive", "fv2d_apply_source",
                      "fv2d_synchronize", "fv2d_device_state", "fv2d_last_error", "fv2d_get_stats",
                      "fv2d_set_profiling", "fv2d_snapshot", "fv2d_snapshot_wait", "fv2d_host_alloc",
-                     "fv2d_host_free", "fv2d_peer_export", "fv2d_peer_connect", "fv2d_peer_connect_local"):
+                     "fv2d_host_free", "fv2d_peer_export", "fv2d_peer_connect", "fv2d_peer_connect_local",
+                     "fv2d_step_host"):
             getattr(L, name).restype = C.c_int
         _LIB = L
     return _LIB
@@ -270,6 +272,19 @@ class Solver:
             return buf[:nsteps]
         self._check(lib().fv2d_step_adaptive(self._h, cfl, nsteps, None), "step_adaptive")
         return None
+
+    def step_host(self, W_in, W_out, dt: float, nsteps: int = 1, layout: int = AOS):
+        """fv2d_step_host: W^0 from host W_in, nsteps fixed-dt steps, result into host
+        W_out (may be W_in); numpy arrays, PinnedArray or raw pointers (ints)."""
+        def ptr(x):
+            if isinstance(x, int):
+                return x
+            arr = x.array if isinstance(x, PinnedArray) else x
+            if arr.shape != self._shape(layout) or arr.dtype != np.float64 or not arr.flags.c_contiguous:
+                raise ValueError(f"host state must be float64 C-contiguous {self._shape(layout)}")
+            return arr.ctypes.data
+        self._check(lib().fv2d_step_host(self._h, C.c_void_p(ptr(W_in)), C.c_void_p(ptr(W_out)), layout, dt, nsteps),
+                    "step_host")
 
     def apply_source(self, dt: float):
         self._check(lib().fv2d_apply_source(self._h, dt), "apply_source")

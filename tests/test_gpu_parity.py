@@ -598,3 +598,56 @@ def test_adaptive_smax_near_ties_and_high_mach(p0):
         W, log = gpu_run(cfg, W0, 6, O.ADAPTIVE, 0.45, flags=flags)
         assert np.array_equal(log, ref.dt_log)
         assert np.array_equal(W, ref.W)
+
+
+@pytest.mark.parametrize("name,nsteps,inplace", [("euler_laxliu3_256", 1, False), ("euler_laxliu3_256", 3, True),
+                                                 ("euler_random_300x200", 1, True),
+                                                 ("euler_sod_wall_y_40x250", 1, False),
+                                                 ("euler_dirichlet_130x70", 2, False),
+                                                 ("adv_dyadic_64", 1, False)])
+def test_step_host_pipelined_same_bits(name, nsteps, inplace):
+    """fv2d_step_host (banded, copy-overlapped host -> host step): the same bits
+    as set_state + step + get_state and as the oracle."""
+    cfg, gen, cflv = CASES[name]
+    W0 = gen()
+    dt = cflv * min((cfg.x1 - cfg.x0) / cfg.nx, (cfg.y1 - cfg.y0) / cfg.ny) / O.smax(cfg, W0)[0]
+    ref = O.run(cfg, W0, nsteps, O.FIXED, dt)
+    with solver_for(cfg) as s:
+        out = W0.copy() if inplace else np.empty_like(W0)
+        s.step_host(out if inplace else W0, out, dt, nsteps)
+        assert np.array_equal(out, ref.W)
+        assert np.array_equal(s.get_state(), ref.W)
+        s.step(dt, 1)  # the context continues from the result (ghost rows, step counter)
+        assert np.array_equal(s.get_state(), O.run(cfg, W0, nsteps + 1, O.FIXED, dt).W)
+
+
+def test_step_host_cfl_violation_returns_w0():
+    """A fixed dt violating eq:CFL_cond: E_CFL and host_out holds W^0 even though
+    the pipelined step already copied bands of W^1 out (and in place)."""
+    cfg, gen, _ = CASES["euler_laxliu3_256"]
+    W0 = gen()
+    dt = 1.5 * (1.0 / 256) / O.smax(cfg, W0)[0]
+    with solver_for(cfg) as s:
+        out = W0.copy()
+        with pytest.raises(fv2d.FV2DError) as ei:
+            s.step_host(out, out, dt, 1)
+        assert ei.value.code == fv2d.E_CFL
+        assert np.array_equal(out, W0)
+
+
+def test_step_host_fallbacks_soa_and_spray():
+    cfg, gen, cflv = CASES["euler_random_300x200"]
+    W0 = gen()
+    dt = 0.4 * (1.5 / 300) / O.smax(cfg, W0)[0]
+    ref = O.run(cfg, W0, 2, O.FIXED, dt)
+    with solver_for(cfg) as s:
+        soa_in = np.ascontiguousarray(W0.transpose(2, 0, 1))
+        soa_out = np.empty_like(soa_in)
+        s.step_host(soa_in, soa_out, dt, 2, layout=fv2d.SOA)
+        assert np.array_equal(soa_out.transpose(1, 2, 0), ref.W)
+    scfg, S0, sdt = spray_case(48)
+    sref = O.run(scfg, S0, 2, O.FIXED, sdt)
+    with solver_for(scfg) as s:
+        out = np.empty_like(S0)
+        s.step_host(S0, out, sdt, 2)
+        assert relerr(out, sref.W) <= 1e-10
