@@ -135,7 +135,7 @@ struct fv2d_ctx {
   bool graph_ready = false;
   int graph_adaptive = -1;
   double graph_dt = 0.0, graph_cfl = 0.0;
-  bool graph_lam_valid = false;
+  int graph_lam_hist = 0;
   const double* graph_dt_log = nullptr;
   // asynchronous output (fv2d_snapshot)
   cudaStream_t out_stream = nullptr;
@@ -166,8 +166,12 @@ struct fv2d_ctx {
   long long dt_log_cap = 0;
   unsigned long long* newton = nullptr;
   double* trig = nullptr;  // sx[nx] cx[nx] sy[ny] cy[ny]
-  double* lam_cache = nullptr;  // spray: Newton warm start, nslabs x H x 4 x pitch
-  bool lam_valid = false;
+  // spray: Newton warm start, two caches of nslabs x H x 4 x pitch: the pass
+  // reading state parity p reads lambda_n from lam_buf[p] and lambda_{n-1} from
+  // lam_buf[1-p] and writes lambda_{n+1} over lambda_{n-1} (a CUDA graph is
+  // captured per parity, and recaptured when lam_hist changes)
+  double* lam_buf[2] = {nullptr, nullptr};
+  int lam_hist = 0;  // valid history entries: 0 (cold start), 1 (lambda_n), 2 (and lambda_{n-1})
   ncclComm_t comm = nullptr;
   bool use_nccl = false;  // nranks > 1, or FV2D_FLAG_NCCL_LOOPBACK (self exchange on 1 rank)
   // FV2D_FLAG_PEER_HALO: halo rows and the CFL max-all-reduce through peer memory
@@ -389,8 +393,10 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.step_dev = reinterpret_cast<long long*>(ctx->dscal + 6);
   a.col_lo = 0;
   a.col_hi = ctx->nx;
-  a.lam_cache = ctx->lam_cache;
-  a.lam_valid = ctx->lam_valid ? 1 : 0;
+  a.lam_in = ctx->lam_buf[p];
+  a.lam_out = ctx->lam_buf[q];
+  a.lam_old = ctx->lam_hist >= 2 ? ctx->lam_buf[q] : nullptr;
+  a.lam_valid = ctx->lam_hist >= 1 ? 1 : 0;
   a.peer_fence = ctx->peer ? 1 : 0;
   if (ctx->peer) a.fused_finalize = 0;
   a.xghost = ctx->xg ? 1 : 0;
@@ -780,7 +786,8 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   if (ctx->dt_log) cudaFree(ctx->dt_log);
   if (ctx->newton) cudaFree(ctx->newton);
   if (ctx->trig) cudaFree(ctx->trig);
-  if (ctx->lam_cache) cudaFree(ctx->lam_cache);
+  for (double* b : ctx->lam_buf)
+    if (b) cudaFree(b);
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   if (ctx->sync) cudaFree(ctx->sync);
@@ -922,7 +929,7 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   CKC(cudaMemset(ctx->newton, 0, sizeof(unsigned long long)));
   if (c.system == FV2D_SPRAY) {
     CKC(cudaMalloc(&ctx->trig, (size_t)(2 * c.nx + 2 * c.ny) * sizeof(double)));
-    CKC(cudaMalloc(&ctx->lam_cache, (size_t)ctx->nslabs * H * 4 * ctx->pitch * sizeof(double)));
+    for (double*& b : ctx->lam_buf) CKC(cudaMalloc(&b, (size_t)ctx->nslabs * H * 4 * ctx->pitch * sizeof(double)));
     trig_table_kernel<<<(c.nx + 255) / 256, 256>>>(ctx->trig, ctx->trig + c.nx, c.nx, c.x0, ctx->dx);
     trig_table_kernel<<<(c.ny + 255) / 256, 256>>>(ctx->trig + 2 * c.nx, ctx->trig + 2 * c.nx + c.ny, c.ny, c.y0,
                                                     ctx->dy);
@@ -1004,7 +1011,7 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->has_state = true;
   ctx->dt_valid = false;
-  ctx->lam_valid = false;
+  ctx->lam_hist = 0;
   ctx->err.clear();
   ctx->err_step = ctx->err_cell = -1;
   return FV2D_OK;
@@ -1291,7 +1298,7 @@ static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double
   ctx->graph_adaptive = adaptive;
   ctx->graph_dt = dt;
   ctx->graph_cfl = cfl;
-  ctx->graph_lam_valid = ctx->lam_valid;
+  ctx->graph_lam_hist = ctx->lam_hist;
   ctx->graph_dt_log = ctx->dt_log;
   return FV2D_OK;
 }
@@ -1315,7 +1322,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
     }
     if (use_graph) {
       if (!ctx->graph_ready || ctx->graph_adaptive != adaptive || ctx->graph_dt != dt || ctx->graph_cfl != cfl ||
-          ctx->graph_lam_valid != ctx->lam_valid || ctx->graph_dt_log != ctx->dt_log) {
+          ctx->graph_lam_hist != ctx->lam_hist || ctx->graph_dt_log != ctx->dt_log) {
         st = capture_graphs(ctx, adaptive, dt, cfl);
         if (st) return st;
       }
@@ -1326,7 +1333,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
       st = issue_step(ctx, p, adaptive, dt, cfl, e1);
       if (st) return st;
     }
-    if (split) ctx->lam_valid = true;
+    if (split) ctx->lam_hist = std::min(2, ctx->lam_hist + 1);
     ctx->steps += 1;
   }
   return FV2D_OK;
@@ -1457,7 +1464,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   CK(cudaStreamWaitEvent(ctx->stream, ev_start, 0));
   ctx->has_state = true;
   ctx->dt_valid = false;
-  ctx->lam_valid = false;
+  ctx->lam_hist = 0;
   ctx->err.clear();
   ctx->err_step = ctx->err_cell = -1;
   ctx->steps = 1;
@@ -1509,10 +1516,15 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   StepArgs b = make_args(ctx, 1 - p);
   for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, p, 0);
   b.step = ctx->steps;
+  // the multipliers of the current state W (parity p) are in lam_buf[p]: warm
+  // start from them, no extrapolation, write back in place (history broken)
+  b.lam_in = ctx->lam_buf[p];
+  b.lam_out = ctx->lam_buf[p];
+  b.lam_old = nullptr;
   dim3 grid((ctx->nx + kSrcThreads - 1) / kSrcThreads, std::min(ctx->H, 65535), ctx->nslabs);
   spray_source_kernel<<<grid, kSrcThreads, 0, ctx->stream>>>(b, dt, 0);
   CKL();
-  ctx->lam_valid = true;
+  ctx->lam_hist = 1;
   fv2d_status st = exchange(ctx, p);
   if (st) return st;
   if (ctx->peer) {

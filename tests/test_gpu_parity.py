@@ -651,3 +651,24 @@ def test_step_host_fallbacks_soa_and_spray():
         out = np.empty_like(S0)
         s.step_host(S0, out, sdt, 2)
         assert relerr(out, sref.W) <= 1e-10
+
+
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_GRAPH])
+def test_spray_warm_start_history_across_standalone_source(flags):
+    """The split source starts Newton from 2 lambda_n - lambda_{n-1} (per-cell
+    caches alternating with the device step counter); a standalone
+    fv2d_apply_source in between breaks the history.  Tolerance parity with the
+    cold-started oracle over the whole sequence."""
+    cfg, W0, dt = spray_case(40)
+    ref = O.run(cfg, W0, 6, O.FIXED, dt).W
+    ref, _ = O.source_step(cfg, ref, dt)
+    ref = O.run(cfg, ref, 7, O.FIXED, dt).W
+    with solver_for(cfg, flags=flags) as s:
+        s.set_state(W0)
+        s.step(dt, 6)
+        s.apply_source(dt)
+        s.step(dt, 7)
+        W = s.get_state()
+        iters = s.stats()["newton_iters"]
+    assert relerr(W, ref) <= 1e-10
+    assert iters > 0
