@@ -202,6 +202,9 @@ def main():
     ap.add_argument("--nranks-x", type=int, default=1,
                     help="N>1: the ranks as a PX x (N/PX) grid of 2-D blocks (E/W ghost columns) instead of y-slabs")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="test mode: every rank on cuda:0 with gloo for the host-side collectives "
+                         "(needs --peer-halo: NCCL refuses two ranks on one GPU); not a scaling measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -220,10 +223,18 @@ def main():
     from paper_1701_05431_b200 import dist as D
     from paper_1701_05431_b200 import fv2d
 
+    if args.shared_gpu:
+        if world > 1 and not args.peer_halo:
+            raise SystemExit("--shared-gpu needs --peer-halo")
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if args.shared_gpu else "cuda"  # device of the max-over-ranks reductions
     system, nx, ny_global, desc = WORKLOADS[args.workload]
     weak = args.workload.startswith("c5")
     ny = ny_global * world if weak else ny_global
@@ -282,7 +293,7 @@ def main():
     s.synchronize()                      # no latched CFL/non-finite error in the timed steps
     kern_ms = st1["step_kernel_ms"] / max(1, st1["step_kernels_timed"])
     launches = st1["kernel_launches"] - st0["kernel_launches"]
-    ms_max, kern_max = D.max_over_ranks([ms, kern_ms], device="cuda")
+    ms_max, kern_max = D.max_over_ranks([ms, kern_ms], device=red_dev)
     cells_total = nx * ny
     value = cells_total * args.steps / (ms_max * 1e-3)
 
@@ -303,7 +314,7 @@ def main():
             s.step_host(ptr, ptr, dt, 1)
         e1.record(stream)
         barrier()
-        (et,) = D.max_over_ranks([e0.elapsed_time(e1)], device="cuda")
+        (et,) = D.max_over_ranks([e0.elapsed_time(e1)], device=red_dev)
         nbytes = W0.size * 8
         e2e = {"value": cells_total * args.e2e_steps / (et * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
@@ -334,7 +345,9 @@ def main():
                        "parallelism": (f"y-slabs x{world}" if px == 1 else f"2-D blocks {px}x{world // px}") + (
                            (" (peer-memory halo + all-reduce)" if peer else " (NCCL halo overlapped + all-reduce)")
                            if world > 1 else ""),
-                       "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % ((i1 - i0) * H * 32 / 1e9)},
+                       "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % ((i1 - i0) * H * 32 / 1e9),
+                       **({"test_mode": "all ranks share cuda:0 (--shared-gpu): not a scaling measurement"}
+                          if args.shared_gpu else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_cell": bpc, "kernel_ms": kern_max, "cells_per_launch": cells_per_launch},

@@ -44,3 +44,30 @@ def test_bench_json_contract_on_gpu():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 1024 * 1024 * 32 and d["e2e"]["value"] > 0
     assert d["config"]["workload"] == "c2_euler_1024"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("px", [1, 2])
+def test_bench_multi_rank_launch_on_one_gpu(px):
+    """The N>1 bench flow under torch.distributed.run (2 ranks), as far as one
+    GPU allows: --shared-gpu puts both ranks on cuda:0 with the peer-memory path
+    (CUDA IPC) and gloo for the host collectives.  One JSON line from rank 0,
+    n_gpus = 2, max-over-ranks timing; y-slabs (px = 1) or 2-D blocks (px = 2)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--peer-halo",
+           "--shared-gpu", "--nranks-x", str(px), "--workload", "c2_euler_1024", "--steps", "10", "--warmup", "3",
+           "--e2e-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["config"]["test_mode"].startswith("all ranks share cuda:0")
+    assert ("2-D blocks 2x1" if px == 2 else "y-slabs x2") in d["config"]["parallelism"]
+    assert d["cpu_baseline"] is None and d["e2e"]["value"] > 0
