@@ -248,20 +248,27 @@ def test_spray_adaptive(flags):
 
 
 # ---------------------------------------------------- full size, sampled (c3)
-def test_full_size_16384_sampled_rows():
-    """BASELINE configs[2] at full size (16384^2, Lax-Liu 3), in the launch
-    configuration bench.py times (fixed dt, fused kernel): one step, then
-    sampled row bands recomputed by the oracle (each cell's stencil is local:
-    a band [j0-1, j1+1) of W^n determines rows [j0, j1) of W^{n+1})."""
-    n = 16384
+@pytest.mark.parametrize("n,api,flags", [(16384, "step", 0), (16384, "step_host", 0),
+                                         (16384, "step", fv2d.FLAG_GHOST_COLUMNS), (8192, "step", 0)])
+def test_full_size_sampled_rows(n, api, flags):
+    """BASELINE configs[2] at full size (16384^2, Lax-Liu 3) in the launch
+    configuration bench.py times (fixed dt, fused kernel; also through the
+    pipelined fv2d_step_host the e2e number uses, and with the 2-D blocks'
+    stored ghost columns), and configs[4]'s 8192^2 per-GPU domain: one step,
+    then sampled row bands recomputed by the oracle (each cell's stencil is
+    local: a band [j0-1, j1+1) of W^n determines rows [j0, j1) of W^{n+1})."""
     cfg = O.Config(nx=n, ny=n, system=O.EULER, param=(G,))
     W0 = inputs.euler_lax_liu3(n, n)
     dt = 0.45 * (1.0 / n) / 2.5
-    with solver_for(cfg) as s:
-        s.set_state(W0)
-        s.step(dt, 1)
-        W1 = s.get_state()
-    for j0 in (0, 4093, 8191, 16376):
+    with solver_for(cfg, flags=flags) as s:
+        if api == "step_host":
+            W1 = np.empty_like(W0)
+            s.step_host(W0, W1, dt, 1)
+        else:
+            s.set_state(W0)
+            s.step(dt, 1)
+            W1 = s.get_state()
+    for j0 in (0, n // 4 - 3, n // 2 - 1, n - 8):
         lo, hi = j0 - 1, j0 + 9
         rows = [r % n for r in range(lo, hi)]
         band = W0[rows]
