@@ -1198,17 +1198,34 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
     at.no_smax = 1;         // adaptive: smax of the post-source state comes from the source pass
   }
   cudaStream_t ls = ctx->launch_stream;
-  // NCCL path for transport-only systems: boundary strips first, halo
-  // exchange on the comm stream overlapped with the interior strips.
-  const int hb = 8;
-  const bool overlap =
-      ctx->use_nccl && !split && !tiled && !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H > 4 * hb && !ctx->xg;
+  // NCCL path for transport-only systems: boundary strips first (rows, and
+  // with ghost columns the west/east column strips too), halo exchange on the
+  // comm stream overlapped with the interior.
+  const int hb = 8, cb = 64;  // boundary rows / columns (even: column cuts are on even columns)
+  const bool overlap = ctx->use_nccl && !split && !tiled && !(ctx->cfg.flags & FV2D_FLAG_NAIVE) &&
+                       ctx->H > 4 * hb && (!ctx->xg || ctx->nx >= 4 * cb);
   if (overlap) {
     StepArgs ab = at, ai = at;
     set_ranges(ab, 0, hb, hb, ctx->H - hb, ctx->H, hb);
     set_ranges(ai, hb, ctx->H - hb, ctx->rps, 0, 0, 1);
     dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, ab);
     CKL();
+    if (ctx->xg) {  // column strips [0, cb) and [ce, nx) of the interior rows
+      const int ce = (ctx->nx - cb) & ~1;
+      StepArgs bw = at, be = at;
+      set_ranges(bw, hb, ctx->H - hb, pick_rps(cb, ctx->H - 2 * hb), 0, 0, 1);
+      set_ranges(be, hb, ctx->H - hb, pick_rps(ctx->nx - ce, ctx->H - 2 * hb), 0, 0, 1);
+      bw.col_lo = 0;
+      bw.col_hi = cb;
+      be.col_lo = ce;
+      be.col_hi = ctx->nx;
+      ai.col_lo = cb;
+      ai.col_hi = ce;
+      dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, bw);
+      CKL();
+      dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, be);
+      CKL();
+    }
     CK(cudaEventRecord(ctx->ev_bnd, ls));
     CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_bnd, 0));
     st = exchange(ctx, 1 - p, ctx->comm_stream);

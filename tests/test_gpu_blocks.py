@@ -175,11 +175,14 @@ def test_ghost_columns_single_context(bc_x, nslabs):
     assert np.array_equal(W, ref.W)
 
 
-@pytest.mark.parametrize("bc_x", [O.BC_PERIODIC, O.BC_WALL])
-def test_ghost_columns_nccl_loopback(bc_x):
+@pytest.mark.parametrize("bc_x,nx,ny", [(O.BC_PERIODIC, 100, 48), (O.BC_WALL, 100, 48), (O.BC_PERIODIC, 300, 80),
+                                        (O.BC_WALL, 258, 72)])
+def test_ghost_columns_nccl_loopback(bc_x, nx, ny):
     """The NCCL column exchange (packed send columns, grouped send/recv, unpack
-    into the ghost columns) as a 1-rank self exchange."""
-    cfg, W0 = euler(100, 48, bc_x, O.BC_PERIODIC, seed=23)
+    into the ghost columns) as a 1-rank self exchange; from nx >= 256 the
+    boundary rows and column strips run first and the exchange overlaps the
+    interior launch on the comm stream."""
+    cfg, W0 = euler(nx, ny, bc_x, O.BC_PERIODIC, seed=23)
     ref = O.run(cfg, W0, 12, O.ADAPTIVE, 0.45)
     W, log = run_single(cfg, W0, 12, O.ADAPTIVE, 0.45, nccl_id=fv2d.nccl_unique_id(),
                         flags=fv2d.FLAG_GHOST_COLUMNS | fv2d.FLAG_NCCL_LOOPBACK)
