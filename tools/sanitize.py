@@ -23,6 +23,17 @@ cases = [
     dict(nx=130, ny=60, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_GRAPH, tiles=(2, 2),
          W=inputs.euler_random(130, 60)),
     dict(nx=130, ny=64, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_NCCL_LOOPBACK, W=inputs.euler_random(130, 64)),
+    # stored ghost columns (the 2-D rank blocks' layout and kernels' xghost mode)
+    dict(nx=126, ny=60, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_GHOST_COLUMNS, nslabs=2,
+         W=inputs.euler_random(126, 60, seed=8)),
+    dict(nx=125, ny=64, system=fv2d.EULER, param=(1.4,), bc_x=fv2d.BC_WALL, flags=fv2d.FLAG_GHOST_COLUMNS,
+         W=inputs.euler_random(125, 64, seed=9)),
+    dict(nx=130, ny=70, system=fv2d.EULER, param=(1.4,), bc_x=fv2d.BC_DIRICHLET, dirichlet=(1.0, 0.1, -0.2, 2.6),
+         flags=fv2d.FLAG_GHOST_COLUMNS | fv2d.FLAG_ONE_CELL, W=inputs.euler_random(130, 70, seed=10)),
+    dict(nx=33, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), flags=fv2d.FLAG_GHOST_COLUMNS,
+         W=inputs.spray_taylor_green(33, 32)),
+    dict(nx=300, ny=80, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_GHOST_COLUMNS | fv2d.FLAG_NCCL_LOOPBACK,
+         W=inputs.euler_random(300, 80, seed=11)),
 ]
 for c in cases:
     W = c.pop("W")
@@ -42,4 +53,15 @@ for c in cases:
         assert np.array_equal(snap.array, W)
         snap.free()
         assert np.all(np.isfinite(out))
+# the pipelined host -> host step (banded H2D / step / D2H on three streams)
+W = inputs.euler_random(256, 160, seed=12)
+with fv2d.Solver(256, 160, fv2d.EULER, param=(1.4,)) as s:
+    s.set_state(W)
+    dt, _ = s.compute_dt(0.4)
+    pin = fv2d.PinnedArray(W.shape)
+    pin.array[:] = W
+    s.step_host(pin, pin, dt, 1)
+    s.step_host(pin, pin, dt, 2)
+    assert np.all(np.isfinite(pin.array))
+    pin.free()
 print("sanitize cases ok")
