@@ -112,7 +112,10 @@ int nvar_of(int system) {
   }
 }
 
-constexpr int kWarps = 4;
+#ifndef FV2D_WARPS
+#define FV2D_WARPS 4  // warps per CTA of the marching kernels (tuning knob)
+#endif
+constexpr int kWarps = FV2D_WARPS;
 
 }  // namespace
 
