@@ -41,7 +41,14 @@ WORKLOADS = {
                                               "periodic, fixed dt checked each step, y-slabs (strong scaling)"),
     "c2_euler_1024": ("euler", 1024, 1024, "BASELINE configs[1]: 2D Euler nVar=4, 1024x1024, Lax-Liu 3"),
     "c5_euler_8192_per_gpu": ("euler", 8192, 8192, "BASELINE configs[4]: 8192^2 cells per GPU (weak scaling)"),
+    "c4_spray_4096": ("spray", 4096, 4096, "BASELINE configs[3]: evaporating spray nVar=6 (eq:Essadki), 4096x4096, "
+                                           "Taylor-Green IC (R16), K=theta=1, the paper's fixed dt (R17), split "
+                                           "source with the NDF reconstruction (S:401-419)"),
 }
+# FP64 peak of the spray source kernel's roofline (bound "alu"): 148 SMs x 64
+# FP64 lanes (measured 64 DFMA/DADD/DMUL per SM per clock, tools/microbench.cu)
+# x 2 flop per DFMA x 1.965 GHz max SM clock (B200_PROFILING.md unit counts)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
 def measured_peaks():
@@ -121,21 +128,52 @@ class ClockSampler:
 
 
 def gen_ic(system, nx, ny, rows):
-    """Lax-Liu 3 in row chunks (bounded temporaries) into one AoS array."""
+    """Lax-Liu 3 (Euler) or the R16 Taylor-Green spray state, in row chunks
+    (bounded temporaries) into one AoS array."""
     from paper_1701_05431_b200 import inputs
     j0, j1 = rows
-    out = np.empty((j1 - j0, nx, 4))
+    nv = 6 if system == "spray" else 4
+    out = np.empty((j1 - j0, nx, nv))
     for a in range(j0, j1, 1024):
         b = min(j1, a + 1024)
-        out[a - j0:b - j0] = inputs.euler_lax_liu3(nx, ny, rows=(a, b), gamma=GAMMA)
+        out[a - j0:b - j0] = (inputs.spray_taylor_green(nx, ny, rows=(a, b)) if system == "spray" else
+                              inputs.euler_lax_liu3(nx, ny, rows=(a, b), gamma=GAMMA))
     return out
 
 
-def cpu_baseline(nx, ny, budget_s=12.0):
+def spray_band_oracle(nx, ny, rows, budget_s, steps=None):
+    """The oracle's spray step (transport + source, cold-start Newton as R19) on a
+    full-width row band of the c4 workload: (cell-updates/s, steps, seconds)."""
+    import oracle as O
+    from paper_1701_05431_b200 import inputs
+    j0 = ny // 2 - rows // 2
+    band = inputs.spray_taylor_green(nx, ny, rows=(j0, j0 + rows))
+    cfg = O.Config(nx=nx, ny=rows, system=O.SPRAY, param=(1.0, 1.0), y0=j0 / ny, y1=(j0 + rows) / ny)
+    s0, _ = O.smax(cfg, band)
+    dt = 0.5 * (1.0 / nx) / s0
+    W = band
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        W = O.transport_step(cfg, W, dt)
+        W, _ = O.source_step(cfg, W, dt)
+        n += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and n >= steps) or (steps is None and el > budget_s):
+            break
+    return nx * rows * n / el, n, el
+
+
+def cpu_baseline(nx, ny, budget_s=12.0, system="euler"):
     """The oracle as it stands (single-threaded C, -O2 -ffp-contract=off) on a
     bounded sample: full-width row bands of the same workload, periodic."""
     import oracle as O
     from paper_1701_05431_b200 import inputs
+    if system == "spray":
+        v, n, el = spray_band_oracle(nx, ny, 8, budget_s)
+        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"{n} spray steps (transport + source, cold-start Newton) on a {nx}x8 full-width row "
+                          f"band of the workload, {el:.1f} s, 1 thread"}
     rows = min(ny, 256)
     band = inputs.euler_lax_liu3(nx, ny, rows=(ny // 2 - rows // 2, ny // 2 + rows // 2), gamma=GAMMA)
     cfg = O.Config(nx=nx, ny=rows, system=O.EULER, param=(GAMMA,), y1=rows / ny)
@@ -161,6 +199,21 @@ def run_reference(args, rank, world):
     system, nx, ny, desc = WORKLOADS[args.workload]
     import oracle as O
     from paper_1701_05431_b200 import inputs
+    if system == "spray":
+        # ~1 M cell-updates/s: a 2-row band keeps the whole run within minutes
+        spray_band_oracle(nx, ny, 2, 0.0, steps=args.warmup)
+        val, n, el = spray_band_oracle(nx, ny, 2, 0.0, steps=args.steps)
+        sample = f"each step = one oracle spray step (transport + source) on a {nx}x2 full-width row band"
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.workload, "description": desc, "nx": nx, "ny": ny,
+                                            "sample_rows": 2},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     # size the band so that warmup + steps take ~60 s of CPU at ~10 M cell-updates/s
     total = max(1, args.steps + args.warmup)
     rows = int(max(2, min(ny, 60e6 / total / nx)))
@@ -250,8 +303,10 @@ def main():
     stream = torch.cuda.current_stream()
     flags = (fv2d.FLAG_NAIVE if args.naive else 0) | (fv2d.FLAG_ONE_CELL if args.one_cell else 0) | \
         (fv2d.FLAG_PEER_HALO if peer else 0)
-    s = fv2d.Solver(nx, ny, fv2d.EULER, param=(GAMMA,), rank=rank, nranks=world, device=local, flags=flags,
-                    nranks_x=px, nccl_id=nccl_id, stream=stream.cuda_stream)
+    spray = system == "spray"
+    s = fv2d.Solver(nx, ny, fv2d.SPRAY if spray else fv2d.EULER, param=(1.0, 1.0) if spray else (GAMMA,),
+                    rank=rank, nranks=world, device=local, flags=flags, nranks_x=px, nccl_id=nccl_id,
+                    stream=stream.cuda_stream)
     if peer:
         handles = [None] * world
         dist.all_gather_object(handles, s.peer_export())
@@ -261,6 +316,8 @@ def main():
         W0 = np.ascontiguousarray(W0[:, i0:i1])
     s.set_state(W0)
     dt, smax0 = s.compute_dt(CFL)    # the paper's constant dt, set at start
+    if spray:
+        dt = 0.5 * min(1.0 / nx, 1.0 / ny) / smax0   # R17
 
     def steps(k):
         if args.adaptive:
@@ -292,8 +349,9 @@ def main():
     s.set_profiling(False)
     s.synchronize()                      # no latched CFL/non-finite error in the timed steps
     kern_ms = st1["step_kernel_ms"] / max(1, st1["step_kernels_timed"])
+    src_ms = st1["source_kernel_ms"] / max(1, st1["source_kernels_timed"])
     launches = st1["kernel_launches"] - st0["kernel_launches"]
-    ms_max, kern_max = D.max_over_ranks([ms, kern_ms], device=red_dev)
+    ms_max, kern_max, src_max = D.max_over_ranks([ms, kern_ms, src_ms], device=red_dev)
     cells_total = nx * ny
     value = cells_total * args.steps / (ms_max * 1e-3)
 
@@ -318,12 +376,14 @@ def main():
         nbytes = W0.size * 8
         e2e = {"value": cells_total * args.e2e_steps / (et * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
-               "api": "fv2d_step_host(host AoS in -> host AoS out, pinned, in place; banded copy/compute overlap)"}
+               "api": "fv2d_step_host(host AoS in -> host AoS out, pinned, in place; " +
+                      ("set_state + step + get_state in sequence for the spray)" if spray else
+                       "banded copy/compute overlap)")}
         del hostbuf
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(nx, ny)
+        cpu = cpu_baseline(nx, ny, system=system)
 
     if rank == 0:
         peak, peak_src = measured_peaks()
@@ -333,6 +393,26 @@ def main():
         kernel = ("fv_step_naive_kernel<Euler>" if args.naive else
                   "fv_step_kernel<Euler> (one cell/lane)" if args.one_cell else "fv_step_pair_kernel<Euler>")
         traffic = ncu_traffic(kernel)
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "bytes_per_cell": bpc, "kernel_ms": kern_max, "cells_per_launch": cells_per_launch}
+        if spray:
+            # the dominant kernel is the source pass: FP64-bound (arithmetic intensity
+            # ~14 flop/B, far above the FP64 ridge of ~5.7 flop/B)
+            kernel = "spray_source_step_kernel (+ fv_step_kernel<Spray> transport)"
+            prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))["spray_source_step_kernel"]
+            fpc = prof["fp64_flops_per_cell"]
+            ach = fpc * cells_per_launch / (src_max * 1e-3) / 1e12
+            roofline = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": ach / FP64_PEAK_TFLOPS, "traffic": prof["dram_bytes_per_launch"],
+                        "peak_source": "derived: 148 SMs x 64 FP64 lanes x 2 flop (DFMA) x 1.965 GHz",
+                        "flops_per_cell": fpc, "flops_per_cell_source": "ncu DFMA/DADD/DMUL counts "
+                        "(profiles/ncu_summary.json), steady state", "kernel_ms": src_max,
+                        "cells_per_launch": cells_per_launch,
+                        "arithmetic_intensity_flop_per_byte": prof["arithmetic_intensity_flop_per_byte"],
+                        "transport_kernel": {"bound": "hbm", "achieved_gbs": achieved, "peak_gbs": peak,
+                                             "frac": achieved / peak, "bytes_per_cell": bpc,
+                                             "kernel_ms": kern_max}}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -342,15 +422,15 @@ def main():
                        "rows_per_gpu": H, "cols_per_gpu": i1 - i0,
                        "mode": "adaptive dt" if args.adaptive else "fixed dt (checked)",
                        "dt": dt, "kernel": kernel,
+                       **({"newton_iters_per_cell_step": (st1["newton_iters"] - st0["newton_iters"]) /
+                           (cells_per_launch * args.steps)} if spray else {}),
                        "parallelism": (f"y-slabs x{world}" if px == 1 else f"2-D blocks {px}x{world // px}") + (
                            (" (peer-memory halo + all-reduce)" if peer else " (NCCL halo overlapped + all-reduce)")
                            if world > 1 else ""),
-                       "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % ((i1 - i0) * H * 32 / 1e9),
+                       "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % ((i1 - i0) * H * bpc / 2 / 1e9),
                        **({"test_mode": "all ranks share cuda:0 (--shared-gpu): not a scaling measurement"}
                           if args.shared_gpu else {})},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_cell": bpc, "kernel_ms": kern_max, "cells_per_launch": cells_per_launch},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -141,6 +141,9 @@ typedef struct {
                               (CUDA events recorded on the context stream around each
                               step-kernel launch), since profiling was enabled */
   int64_t step_kernels_timed; /* number of step-kernel launches in step_kernel_ms */
+  double source_kernel_ms;    /* with profiling on: summed device time of the split spray
+                                 source kernels of steps (not captured in a CUDA graph) */
+  int64_t source_kernels_timed;
 } fv2d_stats;
 
 /* Library version; never fails. */

@@ -200,6 +200,9 @@ struct fv2d_ctx {
   size_t ev_used = 0;
   double prof_ms = 0.0;
   long long prof_n = 0;
+  std::vector<char> ev_tag;     // per event pair: 0 = step kernel, 1 = spray source kernel
+  double prof_src_ms = 0.0;
+  long long prof_src_n = 0;
   std::string err;
   long long err_step = -1, err_cell = -1;
   double err_value = NAN;
@@ -1151,15 +1154,22 @@ static fv2d_status prof_flush(fv2d_ctx* ctx) {
   for (size_t k = 0; k + 1 < ctx->ev_used; k += 2) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, ctx->ev_pool[k], ctx->ev_pool[k + 1]));
-    ctx->prof_ms += ms;
-    ctx->prof_n += 1;
+    if (ctx->ev_tag[k / 2]) {
+      ctx->prof_src_ms += ms;
+      ctx->prof_src_n += 1;
+    } else {
+      ctx->prof_ms += ms;
+      ctx->prof_n += 1;
+    }
   }
   ctx->ev_used = 0;
   return FV2D_OK;
 }
 
-static fv2d_status prof_events(fv2d_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1) {
-  if (ctx->ev_used + 2 > 4096) {
+static fv2d_status prof_events(fv2d_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1, char tag = 0) {
+  // flush only at a step's first pair (tag 0), keeping room for its source pair,
+  // so no pair is ever read before both of its events are recorded
+  if (tag == 0 && ctx->ev_used + 4 > 4096) {
     fv2d_status st = prof_flush(ctx);
     if (st) return st;
   }
@@ -1170,6 +1180,8 @@ static fv2d_status prof_events(fv2d_ctx* ctx, cudaEvent_t* e0, cudaEvent_t* e1) 
   }
   *e0 = ctx->ev_pool[ctx->ev_used];
   *e1 = ctx->ev_pool[ctx->ev_used + 1];
+  if (ctx->ev_tag.size() < ctx->ev_used / 2 + 1) ctx->ev_tag.resize(ctx->ev_used / 2 + 1);
+  ctx->ev_tag[ctx->ev_used / 2] = tag;
   ctx->ev_used += 2;
   return FV2D_OK;
 }
@@ -1271,8 +1283,15 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
     dim3 grid((ctx->nx + kSrcThreads - 1) / kSrcThreads, std::min(ctx->H, 65535), ctx->nslabs);
     StepArgs b = a;
     if (tiled) b.fused_finalize = 0;
+    cudaEvent_t s0 = nullptr, s1 = nullptr;
+    if (e1) {  // profiling, not capturing: time the source kernel on its own
+      st = prof_events(ctx, &s0, &s1, 1);
+      if (st) return st;
+      CK(cudaEventRecord(s0, ls));
+    }
     spray_source_dt_kernel_launch(ctx, b, grid, p);
     CKL();
+    if (s1) CK(cudaEventRecord(s1, ls));
   }
   if (ctx->peer) {
     // the halo rows are already in the neighbours' ghost rows (peer stores of
@@ -1607,6 +1626,8 @@ fv2d_status fv2d_set_profiling(fv2d_ctx* ctx, int32_t enable) {
   ctx->profiling = enable != 0;
   ctx->prof_ms = 0.0;
   ctx->prof_n = 0;
+  ctx->prof_src_ms = 0.0;
+  ctx->prof_src_n = 0;
   return FV2D_OK;
 }
 
@@ -1774,6 +1795,8 @@ fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out) {
   if (st) return st;
   out->step_kernel_ms = ctx->prof_ms;
   out->step_kernels_timed = ctx->prof_n;
+  out->source_kernel_ms = ctx->prof_src_ms;
+  out->source_kernels_timed = ctx->prof_src_n;
   out->steps = ctx->steps;
   out->kernel_launches = ctx->launches;
   unsigned long long ni = 0;

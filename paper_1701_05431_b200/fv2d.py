@@ -39,7 +39,8 @@ class Config(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("kernel_launches", C.c_int64), ("newton_iters", C.c_int64),
-                ("dt", C.c_double), ("step_kernel_ms", C.c_double), ("step_kernels_timed", C.c_int64)]
+                ("dt", C.c_double), ("step_kernel_ms", C.c_double), ("step_kernels_timed", C.c_int64),
+                ("source_kernel_ms", C.c_double), ("source_kernels_timed", C.c_int64)]
 
 
 _LIB = None
@@ -328,4 +329,5 @@ class Solver:
         s = Stats()
         self._check(lib().fv2d_get_stats(self._h, C.byref(s)), "get_stats")
         return {"steps": s.steps, "kernel_launches": s.kernel_launches, "newton_iters": s.newton_iters,
-                "dt": s.dt, "step_kernel_ms": s.step_kernel_ms, "step_kernels_timed": s.step_kernels_timed}
+                "dt": s.dt, "step_kernel_ms": s.step_kernel_ms, "step_kernels_timed": s.step_kernels_timed,
+                "source_kernel_ms": s.source_kernel_ms, "source_kernels_timed": s.source_kernels_timed}

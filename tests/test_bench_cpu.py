@@ -71,3 +71,28 @@ def test_bench_multi_rank_launch_on_one_gpu(px):
     assert d["config"]["test_mode"].startswith("all ranks share cuda:0")
     assert ("2-D blocks 2x1" if px == 2 else "y-slabs x2") in d["config"]["parallelism"]
     assert d["cpu_baseline"] is None and d["e2e"]["value"] > 0
+
+
+def test_reference_arm_spray_workload():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload",
+                        "c4_spray_4096", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "c4_spray_4096"
+
+
+@pytest.mark.gpu
+def test_bench_spray_workload_fp64_roofline():
+    """bench.py --workload c4_spray_4096: the source pass is the dominant kernel;
+    its roofline is FP64 ("alu", TFLOP/s) with the measured arithmetic intensity."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "c4_spray_4096", "--steps", "10",
+                        "--warmup", "3", "--e2e-steps", "1"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    rf = d["roofline"]
+    assert rf["bound"] == "alu" and rf["unit"] == "TFLOP/s" and 0 < rf["frac"] < 1
+    assert rf["arithmetic_intensity_flop_per_byte"] > 5.7        # above the FP64 ridge
+    assert rf["transport_kernel"]["bound"] == "hbm"
+    assert d["value"] > 1e9 and d["e2e"]["value"] > 0 and d["cpu_baseline"]["value"] > 0
+    assert 0.5 < d["config"]["newton_iters_per_cell_step"] < 3
