@@ -679,3 +679,23 @@ def test_spray_warm_start_history_across_standalone_source(flags):
         iters = s.stats()["newton_iters"]
     assert relerr(W, ref) <= 1e-10
     assert iters > 0
+
+
+def test_spray_long_trajectory_300_steps():
+    """300 fixed-dt spray steps (R16 IC, 96^2): the extrapolated warm start
+    (2 lambda_n - lambda_{n-1}) over a long history stays within tolerance of the
+    cold-started oracle, and every cell stays realizable."""
+    cfg, W0, dt = spray_case(96)
+    ref = O.run(cfg, W0, 300, O.FIXED, dt)
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        s.step(dt, 300)
+        W = s.get_state()
+        iters = s.stats()["newton_iters"]
+    assert relerr(W, ref.W) <= 1e-10
+    m0, m1, m2, m3 = (W[..., k] for k in range(4))
+    assert np.all(m3 <= m2) and np.all(m2 <= m1) and np.all(m1 <= m0) and np.all(m3 > 0)
+    assert np.all(m1 * m1 <= m0 * m2) and np.all(m2 * m2 <= m1 * m3)
+    # the extrapolation error is O(dt^2): ~2 Newton iterations per cell-step at this
+    # coarse mesh's dt (5e-3), ~1.0 at c4's 1.2e-4 (tools/longrun.py)
+    assert iters / (96 * 96 * 300) < 3

@@ -1,7 +1,7 @@
 """Long runs at full size (evidence beyond the parity tests):
 c3 16384^2 Euler Lax-Liu 3, 1000 fixed-dt steps: no CFL/admissibility error,
 sum(W) conserved (exact sums with math.fsum per row, periodic, S = 0);
-c4 4096^2 spray, 100 fixed-dt steps: realizable moments everywhere
+c4 4096^2 spray, 1000 fixed-dt steps: realizable moments everywhere
 (positivity, monotonicity, Hankel), total m0 decays (evaporation).
 JSON lines."""
 import json
@@ -42,7 +42,7 @@ def euler(n=16384, steps=1000):
             "rho_min": float(rho.min()), "rho_max": float(rho.max()), "finite": bool(np.isfinite(W).all())}
 
 
-def spray(n=4096, steps=100):
+def spray(n=4096, steps=1000):
     W0 = inputs.spray_taylor_green(n, n)
     with fv2d.Solver(n, n, fv2d.SPRAY, param=(1.0, 1.0)) as s:
         s.set_state(W0)
