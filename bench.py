@@ -7,10 +7,13 @@ cells, Lax-Liu configuration 3 (synthetic, seeded/analytic), periodic, the
 paper's constant dt checked every step, y-slabs over N GPUs
 (strong scaling).  A "step" is one pass of the whole hot path: CFL reduction
 (fused check), x/y Lax-Friedrichs fluxes, conservative update (+ halo exchange
-and max-all-reduce for N > 1).  The state (2 x 8.6 GB) is far larger than L2,
-so no flush is needed between steps.
+and max-all-reduce for N > 1: by default fused into the step kernel over peer
+memory, --nccl for the NCCL baseline).  The state (2 x 8.6 GB) is far larger
+than L2, so no flush is needed between steps.  --workload c4_spray_4096 times
+the spray (BASELINE configs[3]) with the source pass's FP64 roofline.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload ...] [--nranks-x PX] [--nccl]
 
 Prints ONE JSON line on rank 0.
 """
@@ -250,14 +253,17 @@ def main():
     ap.add_argument("--naive", action="store_true", help="paper's one-thread-per-cell kernel (baseline)")
     ap.add_argument("--one-cell", action="store_true", help="one-cell-per-lane fused kernel (default: two)")
     ap.add_argument("--peer-halo", action="store_true",
-                    help="N>1: halo rows and the CFL all-reduce through peer memory (CUDA IPC) instead of NCCL")
+                    help="N>1: peer-memory path (the default for N>1; kept for compatibility)")
+    ap.add_argument("--nccl", action="store_true",
+                    help="N>1: the NCCL baseline (halo send/recv overlapped with the interior, ncclAllReduce) "
+                         "instead of the fused peer-memory path")
     ap.add_argument("--adaptive", action="store_true", help="adaptive dt (smax reduced in the epilogue)")
     ap.add_argument("--nranks-x", type=int, default=1,
                     help="N>1: the ranks as a PX x (N/PX) grid of 2-D blocks (E/W ghost columns) instead of y-slabs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--shared-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 with gloo for the host-side collectives "
-                         "(needs --peer-halo: NCCL refuses two ranks on one GPU); not a scaling measurement")
+                         "(peer-memory path only: NCCL refuses two ranks on one GPU); not a scaling measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -277,8 +283,8 @@ def main():
     from paper_1701_05431_b200 import fv2d
 
     if args.shared_gpu:
-        if world > 1 and not args.peer_halo:
-            raise SystemExit("--shared-gpu needs --peer-halo")
+        if world > 1 and args.nccl:
+            raise SystemExit("--shared-gpu needs the peer-memory path (NCCL refuses two ranks on one GPU)")
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
@@ -296,21 +302,43 @@ def main():
         raise SystemExit(f"{nx}x{ny} cells do not split into {px}x{world // px} blocks")
     j0, j1, i0, i1 = D.block_of(rank, px, world // px, nx, ny)
     H = j1 - j0
-    nccl_id = None
-    peer = world > 1 and args.peer_halo
-    if world > 1 and not peer:
-        nccl_id = D.broadcast_bytes(fv2d.nccl_unique_id() if rank == 0 else None)
+    # N > 1: the fused peer-memory path by default (each step ONE kernel: flux,
+    # update, halo rows/columns stored into the neighbours' ghost cells over
+    # NVLink, CFL max-all-reduce by system-scope atomics in its last CTA); the
+    # NCCL path is the baseline (--nccl) and the fallback if CUDA IPC between
+    # the ranks fails (decided collectively, so every rank takes the same path)
+    peer = world > 1 and not args.nccl
     stream = torch.cuda.current_stream()
-    flags = (fv2d.FLAG_NAIVE if args.naive else 0) | (fv2d.FLAG_ONE_CELL if args.one_cell else 0) | \
-        (fv2d.FLAG_PEER_HALO if peer else 0)
     spray = system == "spray"
-    s = fv2d.Solver(nx, ny, fv2d.SPRAY if spray else fv2d.EULER, param=(1.0, 1.0) if spray else (GAMMA,),
-                    rank=rank, nranks=world, device=local, flags=flags, nranks_x=px, nccl_id=nccl_id,
-                    stream=stream.cuda_stream)
+    base_flags = (fv2d.FLAG_NAIVE if args.naive else 0) | (fv2d.FLAG_ONE_CELL if args.one_cell else 0)
+
+    def make_solver(use_peer):
+        nid = None
+        if world > 1 and not use_peer:
+            nid = D.broadcast_bytes(fv2d.nccl_unique_id() if rank == 0 else None)
+        return fv2d.Solver(nx, ny, fv2d.SPRAY if spray else fv2d.EULER, param=(1.0, 1.0) if spray else (GAMMA,),
+                           rank=rank, nranks=world, device=local,
+                           flags=base_flags | (fv2d.FLAG_PEER_HALO if use_peer else 0), nranks_x=px,
+                           nccl_id=nid, stream=stream.cuda_stream)
+
+    s = None
     if peer:
-        handles = [None] * world
-        dist.all_gather_object(handles, s.peer_export())
-        s.peer_connect(b"".join(handles))
+        ok = 1.0
+        try:
+            s = make_solver(True)
+            handles = [None] * world
+            dist.all_gather_object(handles, s.peer_export())
+            s.peer_connect(b"".join(handles))
+        except fv2d.FV2DError as e:
+            print(f"rank {rank}: peer-memory path unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
+            ok = 0.0
+        (neg_ok,) = D.max_over_ranks([-ok], device="cpu" if args.shared_gpu else "cuda")
+        if -neg_ok < 1.0:  # some rank failed: all take the NCCL path
+            if s is not None:
+                s.close()
+            s, peer = None, False
+    if s is None:
+        s = make_solver(False)
     W0 = gen_ic(system, nx, ny, (j0, j1))
     if px > 1:
         W0 = np.ascontiguousarray(W0[:, i0:i1])
@@ -425,7 +453,8 @@ def main():
                        **({"newton_iters_per_cell_step": (st1["newton_iters"] - st0["newton_iters"]) /
                            (cells_per_launch * args.steps)} if spray else {}),
                        "parallelism": (f"y-slabs x{world}" if px == 1 else f"2-D blocks {px}x{world // px}") + (
-                           (" (peer-memory halo + all-reduce)" if peer else " (NCCL halo overlapped + all-reduce)")
+                           (" (peer memory: halo stores + all-reduce fused in the step kernel)" if peer else
+                            " (NCCL halo overlapped + all-reduce)")
                            if world > 1 else ""),
                        "l2": "state 2 x %.1f GB >> 126 MB L2, no flush needed" % ((i1 - i0) * H * bpc / 2 / 1e9),
                        **({"test_mode": "all ranks share cuda:0 (--shared-gpu): not a scaling measurement"}

@@ -95,6 +95,9 @@ typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
                                         nranks == 1 (self send/recv; needs an id from
                                         fv2d_nccl_unique_id); exercises the multi-GPU
                                         plumbing on one device */
+#define FV2D_FLAG_PEER_SPLIT 0x100u  /* peer-memory path with the CFL all-reduce and the finalize
+                                        as two small kernels after the step kernel instead of
+                                        inside its last CTA (the default: one kernel per step) */
 #define FV2D_FLAG_GHOST_COLUMNS 0x80u /* store x-ghost columns and route the x-neighbour data
                                         through them exactly as for 2-D rank blocks
                                         (nranks_x > 1, where this is implied), even with

@@ -1206,6 +1206,15 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
   a.cfl = cfl;
   a.step = ctx->steps;
   if (ctx->use_nccl || tiled) a.fused_finalize = 0;
+  // peer-memory path, one launch per pass: the pass's last CTA does the
+  // max-all-reduce over the ranks and the finalize (StepArgs::peer_fused)
+  const bool peer_fused = ctx->peer && !tiled && !(ctx->cfg.flags & FV2D_FLAG_PEER_SPLIT);
+  if (peer_fused) {
+    a.fused_finalize = 1;
+    a.peer_fused = 1;
+    a.peer = ctx->pa;
+    a.peer_epoch = ctx->epoch++;
+  }
   StepArgs at = a;  // transport pass
   if (split) {
     at.fuse_source = 0;
@@ -1293,7 +1302,10 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
     CKL();
     if (s1) CK(cudaEventRecord(s1, ls));
   }
-  if (ctx->peer) {
+  if (peer_fused) {
+    // nothing left: halo rows/columns were stored into the neighbours' ghost
+    // cells and [smax, status] all-reduced by the pass itself
+  } else if (ctx->peer) {
     // the halo rows are already in the neighbours' ghost rows (peer stores of
     // the step kernel); reduce [smax, status] over the ranks through peer memory
     st = peer_collective(ctx, ls);

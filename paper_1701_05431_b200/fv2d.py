@@ -21,6 +21,7 @@ AOS, SOA = 0, 1
 FLAG_NAIVE, FLAG_SPLIT_SOURCE, FLAG_ONE_CELL, FLAG_NCCL_LOOPBACK, FLAG_FUSE_SOURCE, FLAG_GRAPH, FLAG_PEER_HALO = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
 FLAG_GHOST_COLUMNS = 0x80
+FLAG_PEER_SPLIT = 0x100
 PEER_HANDLE_BYTES = 192
 NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
 _NAMES = {OK: "OK", E_ARG: "E_ARG", E_CFL: "E_CFL", E_NONFINITE: "E_NONFINITE", E_RECON: "E_RECON",

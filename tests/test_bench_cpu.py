@@ -59,7 +59,7 @@ def test_bench_multi_rank_launch_on_one_gpu(px):
     port = sk.getsockname()[1]
     sk.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--peer-halo",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2",
            "--shared-gpu", "--nranks-x", str(px), "--workload", "c2_euler_1024", "--steps", "10", "--warmup", "3",
            "--e2e-steps", "1"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)

@@ -529,15 +529,18 @@ def _peer_group_run(cfg, W0, P, nsteps, mode, value, flags=0):
     return np.concatenate(out, axis=0), logs
 
 
-@pytest.mark.parametrize("P,bc_y", [(2, O.BC_PERIODIC), (3, O.BC_PERIODIC), (4, O.BC_WALL), (2, O.BC_WALL)])
-def test_peer_memory_halo_and_allreduce_bitwise(P, bc_y):
+@pytest.mark.parametrize("P,bc_y,flags", [(2, O.BC_PERIODIC, 0), (3, O.BC_PERIODIC, 0), (4, O.BC_WALL, 0),
+                                          (2, O.BC_WALL, 0), (3, O.BC_PERIODIC, fv2d.FLAG_PEER_SPLIT),
+                                          (4, O.BC_WALL, fv2d.FLAG_PEER_SPLIT)])
+def test_peer_memory_halo_and_allreduce_bitwise(P, bc_y, flags):
     """FV2D_FLAG_PEER_HALO: boundary rows stored by the step kernel straight into
     the neighbours' ghost rows, CFL max-all-reduce through peer-memory atomics and
-    an arrival counter -- no NCCL.  Same bits and dt sequence as the oracle."""
+    an arrival counter in the step kernel's last CTA (or, FLAG_PEER_SPLIT, in two
+    small kernels after it) -- no NCCL.  Same bits and dt sequence as the oracle."""
     cfg = O.Config(nx=150, ny=96, system=O.EULER, param=(G,), bc_y=bc_y)
     W0 = inputs.euler_random(150, 96, seed=40 + P)
     ref = O.run(cfg, W0, 25, O.ADAPTIVE, 0.45)
-    W, logs = _peer_group_run(cfg, W0, P, 25, O.ADAPTIVE, 0.45)
+    W, logs = _peer_group_run(cfg, W0, P, 25, O.ADAPTIVE, 0.45, flags=flags)
     for lg in logs:
         assert np.array_equal(lg, ref.dt_log)
     assert np.array_equal(W, ref.W)
