@@ -6,7 +6,9 @@
  * Checks, through the ABI only: a constant Euler state is preserved exactly
  * (consistency of eq:VF_scheme); sum(W) is conserved to round-off on a
  * periodic random state; a fixed dt above the CFL bound is rejected
- * with FV2D_E_CFL and the state is left at W^k.  Exit code 0 = ok. */
+ * with FV2D_E_CFL and the state is left at W^k; the host-resident
+ * step fv2d_step_host (pipelined over row bands) gives the same bits as
+ * set_state + step + get_state.  Exit code 0 = ok. */
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -102,6 +104,19 @@ int main(void) {
     fprintf(stderr, "CFL error did not leave W^0 (step %lld)\n", (long long)step);
     return 1;
   }
+  /* 4. fv2d_step_host (host -> 3 steps -> host, in place) == set_state + step + get_state */
+  CHECK(fv2d_set_state(ctx, W, FV2D_AOS));
+  CHECK(fv2d_compute_dt(ctx, 0.45, &dt, &smax));
+  CHECK(fv2d_step(ctx, dt, 3));
+  CHECK(fv2d_get_state(ctx, out, FV2D_AOS));
+  double* hs = malloc(sizeof(double) * nx * ny * nv);
+  memcpy(hs, W, sizeof(double) * nx * ny * nv);
+  CHECK(fv2d_step_host(ctx, hs, hs, FV2D_AOS, dt, 3));
+  if (memcmp(hs, out, sizeof(double) * nx * ny * nv) != 0) {
+    fprintf(stderr, "fv2d_step_host differs from set_state + step + get_state\n");
+    return 1;
+  }
+  free(hs);
   printf("c_client ok: dt0=%.6g smax=%.6g, CFL error '%s' at cell %lld\n", dtlog[0], smax, msg, (long long)cell);
   fv2d_destroy(ctx);
   free(W);
