@@ -404,9 +404,8 @@ def main():
         nbytes = W0.size * 8
         e2e = {"value": cells_total * args.e2e_steps / (et * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
-               "api": "fv2d_step_host(host AoS in -> host AoS out, pinned, in place; " +
-                      ("set_state + step + get_state in sequence for the spray)" if spray else
-                       "banded copy/compute overlap)")}
+               "api": "fv2d_step_host(host AoS in -> host AoS out, pinned, in place; banded copy/compute overlap" +
+                      ("; a new W^0 each step, so the source's Newton starts cold)" if spray else ")")}
         del hostbuf
 
     cpu = None

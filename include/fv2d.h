@@ -232,10 +232,10 @@ fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out);
 /* Host-resident stepping: W^0 = host_in (as fv2d_set_state), nsteps steps of
  * the constant dt checked every step (as fv2d_step), host_out = the result (as
  * fv2d_get_state); synchronous.  Same bits as those three calls.  For a
- * single-rank, single-slab transport-only context (advection, Euler; y-slab
- * layout) with layout FV2D_AOS the first step is pipelined over row bands:
- * band b is copied host->device and converted while band b-1 is stepped and
- * band b-2 is converted back and copied device->host, so the two copy
+ * single-rank, single-slab context (y-slab layout; the spray with its split
+ * source pass run per band) with layout FV2D_AOS the first step is pipelined
+ * over row bands: band b is copied host->device and converted while band b-1
+ * is stepped and band b-2 is converted back and copied device->host, so the two copy
  * directions and the kernels overlap (the bands next to the periodic/wall
  * y-boundary are stepped last, after the ghost rows are filled).  Other
  * contexts run the three calls in sequence.  host_out may equal host_in.

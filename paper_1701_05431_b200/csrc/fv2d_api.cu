@@ -1462,11 +1462,16 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   CK(cudaMemcpyAsync(ctx->dscal, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->done, 0, sizeof(unsigned int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dt_dev, 0, sizeof(double), ctx->stream));
+  ctx->lam_hist = 0;  // a new W^0: the spray source starts Newton cold (R19)
   StepArgs a = make_args(ctx, 0);
   a.adaptive = 0;
   a.dt = dt;
   a.step = 0;
   a.fused_finalize = 0;
+  const bool spray = ctx->cfg.system == FV2D_SPRAY;  // split source pass per band after its transport
+  StepArgs at = a;
+  at.fuse_source = 0;
+  at.no_smax = 1;
   StepArgs hf = make_args(ctx, 1);  // halo targets of parity 0 (as after_set_state)
   hf.slab[0].in = row_ptr(ctx, 0, 0, 0);
   auto convert_in = [&](int b) -> fv2d_status {
@@ -1478,10 +1483,18 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
     return FV2D_OK;
   };
   auto step_band = [&](int b) -> fv2d_status {
-    StepArgs t = a;
+    StepArgs t = at;
     set_ranges(t, lo(b), hi(b), pick_rps(nx, hi(b) - lo(b)), 0, 0, 1);
     dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, t);
     CKL();
+    if (spray) {
+      StepArgs sb = a;
+      sb.src_row_lo = lo(b);
+      sb.src_row_hi = hi(b);
+      dim3 grid((nx + kSrcThreads - 1) / kSrcThreads, std::min(hi(b) - lo(b), 65535), 1);
+      spray_source_dt_kernel_launch(ctx, sb, grid, 0);
+      CKL();
+    }
     dev_to_aos_kernel<<<148 * 2, 256, 0, ctx->stream>>>(row_ptr(ctx, 0, 1, lo(b)), ctx->staging_out + row_doubles * lo(b),
                                                         nv, nx, hi(b) - lo(b), ctx->pitch, ctx->rs);
     CKL();
@@ -1515,7 +1528,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   CK(cudaStreamWaitEvent(ctx->stream, ev_start, 0));
   ctx->has_state = true;
   ctx->dt_valid = false;
-  ctx->lam_hist = 0;
+  ctx->lam_hist = spray ? 1 : 0;  // lambda_1 of every cell is in lam_buf[1]
   ctx->err.clear();
   ctx->err_step = ctx->err_cell = -1;
   ctx->steps = 1;
@@ -1530,7 +1543,7 @@ fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_ou
   if (ctx->peer && !ctx->peer_connected) return set_err(ctx, FV2D_E_STATE, "peer halo: call fv2d_peer_connect first");
   CK(cudaSetDevice(ctx->cfg.device));
   const bool pipelined = layout == FV2D_AOS && nsteps >= 1 && ctx->cfg.nranks == 1 && ctx->nslabs == 1 &&
-                         !ctx->xg && !ctx->use_nccl && !ctx->peer && ctx->cfg.system != FV2D_SPRAY &&
+                         !ctx->xg && !ctx->use_nccl && !ctx->peer && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE) &&
                          !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H >= 128;
   fv2d_status st;
   if (pipelined) {

@@ -663,6 +663,20 @@ def test_step_host_fallbacks_soa_and_spray():
         assert relerr(out, sref.W) <= 1e-10
 
 
+@pytest.mark.parametrize("nsteps", [1, 4])
+def test_step_host_pipelined_spray(nsteps):
+    """The spray through the pipelined host step: per band, transport then the
+    split source pass on the band's rows; the Newton history continues after it."""
+    cfg, S0, dt = spray_case(160)
+    ref = O.run(cfg, S0, nsteps + 2, O.FIXED, dt)
+    with solver_for(cfg) as s:
+        out = S0.copy()
+        s.step_host(out, out, dt, nsteps)
+        assert relerr(out, O.run(cfg, S0, nsteps, O.FIXED, dt).W) <= 1e-12 * nsteps
+        s.step(dt, 2)
+        assert relerr(s.get_state(), ref.W) <= 1e-10
+
+
 @pytest.mark.parametrize("flags", [0, fv2d.FLAG_GRAPH])
 def test_spray_warm_start_history_across_standalone_source(flags):
     """The split source starts Newton from 2 lambda_n - lambda_{n-1} (per-cell
