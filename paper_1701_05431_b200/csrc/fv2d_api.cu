@@ -327,18 +327,36 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
   }
 }
 
-// Strip height of a marching-kernel launch over ncols x nrows cells: ~2 waves
-// of 3 CTAs per SM for large launches (128 rows: 1.6% halo-row overhead), down
-// to 4 rows for small ones, where the serial march of a strip (latency), not
-// bandwidth, bounds the launch.
+// Strip height of a marching-kernel launch over ncols x nrows cells.  A CTA
+// marches one strip of rps rows (+2 halo rows) of kWarps x 62 columns; the
+// launch has C x S CTAs (C column blocks, S = ceil(nrows/rps) strips) of which
+// 148 x 3 are resident at a time.  The cost model ceil(C*S / 444) * (rps + 2)
+// (waves x rows marched per CTA) is minimised over S with rps <= 128 (longer
+// strips measured slower) and rps >= 4: it avoids a nearly empty last wave
+// (e.g. a 16384 x 2048 slab, the 8-GPU share of c3: 16 strips = 1072 CTAs =
+// 2.4 waves, vs 19 strips = 2.9 waves) and gives small domains one wave of
+// short strips (latency-bound: 1024^2 -> rps 12).
 int pick_rps(int ncols, int nrows) {
   static const int rps_max = getenv("FV2D_RPS_MAX") ? atoi(getenv("FV2D_RPS_MAX")) : 128;  // tuning knob
-  const long long colblocks = ((ncols + 62) / 62 + kWarps - 1) / kWarps;
-  static const int rps_force = getenv("FV2D_RPS") ? atoi(getenv("FV2D_RPS")) : 0;  // tuning knob
+  static const int rps_force = getenv("FV2D_RPS") ? atoi(getenv("FV2D_RPS")) : 0;          // tuning knob
   if (rps_force > 0) return std::min(rps_force, std::max(1, nrows));
-  static const int waves = getenv("FV2D_RPS_WAVES") ? atoi(getenv("FV2D_RPS_WAVES")) : 2;  // tuning knob
-  const long long rps = colblocks * nrows / (148 * 3 * std::max(1, waves));
-  return (int)std::max<long long>(4, std::min<long long>(rps_max, rps));
+  const long long C = ((ncols + 62) / 62 + kWarps - 1) / kWarps;
+  const long long slots = 148LL * 3;
+  const int s_min = std::max(1, (nrows + rps_max - 1) / rps_max);
+  const int s_max = std::max(s_min, nrows / 4);
+  long long best_cost = -1;
+  int best_rps = std::min(nrows, rps_max);
+  for (int S = s_min; S <= s_max; ++S) {
+    const int rps = (nrows + S - 1) / S;
+    if (rps < 4 && S > s_min) break;
+    if ((nrows + rps - 1) / rps != S) continue;  // same rps as a smaller S
+    const long long cost = ((C * S + slots - 1) / slots) * (rps + 2);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_rps = rps;
+    }
+  }
+  return std::max(1, best_rps);
 }
 
 // Row ranges of a marching-kernel launch (see StepArgs).
