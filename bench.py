@@ -323,17 +323,26 @@ def main():
 
     s = None
     if peer:
-        ok = 1.0
+        # every rank reaches every collective below whatever fails where
+        h = None
         try:
             s = make_solver(True)
-            handles = [None] * world
-            dist.all_gather_object(handles, s.peer_export())
-            s.peer_connect(b"".join(handles))
+            h = s.peer_export()
         except fv2d.FV2DError as e:
-            print(f"rank {rank}: peer-memory path unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
-            ok = 0.0
+            print(f"rank {rank}: peer-memory path unavailable ({e})", file=sys.stderr, flush=True)
+        handles = [None] * world
+        dist.all_gather_object(handles, h)
+        ok = 1.0 if all(x is not None for x in handles) else 0.0
+        if ok:
+            try:
+                s.peer_connect(b"".join(handles))
+            except fv2d.FV2DError as e:
+                print(f"rank {rank}: peer_connect failed ({e})", file=sys.stderr, flush=True)
+                ok = 0.0
         (neg_ok,) = D.max_over_ranks([-ok], device="cpu" if args.shared_gpu else "cuda")
         if -neg_ok < 1.0:  # some rank failed: all take the NCCL path
+            if rank == 0:
+                print("peer-memory path unavailable on some rank: using NCCL", file=sys.stderr, flush=True)
             if s is not None:
                 s.close()
             s, peer = None, False
