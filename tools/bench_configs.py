@@ -89,5 +89,13 @@ if __name__ == "__main__":
         run("c4_spray_4096_split", fv2d.SPRAY, n, W, 10, 3, param=(1.0, 1.0), fixed_dt=fd)
         run("c4_spray_4096_fused", fv2d.SPRAY, n, W, 10, 3, param=(1.0, 1.0), fixed_dt=fd,
             flags=fv2d.FLAG_FUSE_SOURCE)
+    if want("paper"):
+        # the paper's own workloads (context: PAPER.md 889-900 Euler 16384^2 x 50 iterations in
+        # 61 s on 4 CPU workers + 4 GPUs; 1063-1071 spray 200^2 x 100 iterations in 5.81 s)
+        n = 200
+        W = inputs.spray_taylor_green(n, n)
+        fd = lambda smax: 0.5 * (1.0 / n) / smax
+        run("paper_spray_200_100it", fv2d.SPRAY, n, W, 100, 3, param=(1.0, 1.0), fixed_dt=fd)
+        run("paper_euler_16384_50it", fv2d.EULER, 16384, euler_ic(16384), 50, 3)
     if want("c5"):
         run("c5_euler_8192", fv2d.EULER, 8192, euler_ic(8192), 100, 5)
