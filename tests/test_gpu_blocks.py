@@ -203,3 +203,42 @@ def test_ghost_columns_graph_and_spray():
     sref = O.run(scfg, S0, 4, O.FIXED, dt)
     SW, _ = run_single(scfg, S0, 4, O.FIXED, dt, flags=fv2d.FLAG_GHOST_COLUMNS)
     assert relerr(SW, sref.W) <= 1e-10
+
+
+def _random_block_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    while True:
+        px, py = int(rng.integers(1, 5)), int(rng.integers(1, 3))
+        if 2 <= px * py <= 8:
+            break
+    wl, hl = int(rng.integers(2, 70)), int(rng.integers(3, 40))
+    nx, ny = px * wl, py * hl
+    system = O.EULER if rng.random() < 0.7 else O.ADVECTION
+    bcs = [O.BC_PERIODIC, O.BC_DIRICHLET] + ([O.BC_WALL] if system == O.EULER else [])
+    bc_x, bc_y = int(rng.choice(bcs)), int(rng.choice(bcs))
+    flags = int(rng.choice([0, 0, fv2d.FLAG_ONE_CELL, fv2d.FLAG_NAIVE, fv2d.FLAG_PEER_SPLIT]))
+    if system == O.EULER:
+        cfg = O.Config(nx=nx, ny=ny, system=O.EULER, param=(G,), bc_x=bc_x, bc_y=bc_y, x1=nx / ny,
+                       dirichlet=(1.1, 0.2, -0.1, 2.4))
+        W0 = inputs.euler_random(nx, ny, seed=seed)
+    else:
+        a = (float(rng.choice([-1.0, 0.5, 1.0])), float(rng.choice([-0.75, 0.25, 1.0])))
+        cfg = O.Config(nx=nx, ny=ny, system=O.ADVECTION, param=a, bc_x=bc_x, bc_y=bc_y, x1=nx / ny,
+                       dirichlet=(0.375,))
+        W0 = inputs.advection_dyadic(nx, ny, seed=seed)
+    return cfg, W0, px, py, flags
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_randomized_block_grids_bitwise(seed):
+    """Random block grids (1..4 x 1..2 ranks), block sizes (2..69 x 3..39 cells,
+    odd and even), systems, boundary conditions, kernels and the fused/split
+    peer all-reduce: bitwise the oracle, identical dt logs."""
+    cfg, W0, px, py, flags = _random_block_case(seed)
+    ref = O.run(cfg, W0, 12, O.ADAPTIVE, 0.4, raise_on_error=False)
+    if ref.status != O.OK:
+        pytest.skip(f"oracle status {ref.status} for this random state")
+    W, logs = run_blocks(cfg, W0, px, py, 12, O.ADAPTIVE, 0.4, flags=flags)
+    for lg in logs:
+        assert np.array_equal(lg, ref.dt_log), (px, py, cfg.nx, cfg.ny, flags)
+    assert np.array_equal(W, ref.W), (px, py, cfg.nx, cfg.ny, flags)
