@@ -467,10 +467,18 @@ struct LaunchStep {
       if constexpr (Sys::NV == 6) {
         const int cols = 30 * kWarps;
         dim3 grid((a.col_hi - a.col_lo + cols - 1) / cols, total_strips(a), ctx->nslabs);
-        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
-        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
-        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
-        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ctx->launch_stream>>>(a);
+        cudaStream_t ls = ctx->launch_stream;
+        if (a.fuse_source) {
+          if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
+          if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
+          if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
+          if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
+        } else {  // split source: the transport pass without the fused-source code
+          if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
+          if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
+          if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
+          if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
+        }
       } else if (ctx->cfg.flags & FV2D_FLAG_ONE_CELL) {
         const int cols = 30 * kWarps;
         dim3 grid((a.col_hi - a.col_lo + cols - 1) / cols, total_strips(a), ctx->nslabs);
@@ -553,6 +561,12 @@ struct Preload {
     t(touch(fv_step_kernel<Sys, true, true, kWarps, 4>));
     t(touch(fv_step_kernel<Sys, false, false, kWarps, 4>));
     t(touch(fv_step_kernel<Sys, false, true, kWarps, 4>));
+    if constexpr (Sys::NV == 6) {
+      t(touch(fv_step_kernel<Sys, true, false, kWarps, 4, false>));
+      t(touch(fv_step_kernel<Sys, true, true, kWarps, 4, false>));
+      t(touch(fv_step_kernel<Sys, false, false, kWarps, 4, false>));
+      t(touch(fv_step_kernel<Sys, false, true, kWarps, 4, false>));
+    }
     t(touch(finalize_kernel));
     t(touch(peer_collective_kernel));
     t(touch(promote_pending_kernel));
