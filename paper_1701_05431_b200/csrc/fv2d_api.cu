@@ -439,19 +439,24 @@ void dispatch(int system, Args&&... args) {
   }
 }
 
-template <class Sys, int D, bool XPER, bool ADAPT>
+template <class Sys, int D, int XM, bool ADAPT>
 void launch_pair_1(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
   // (the dynamic shared-memory opt-in was set once at fv2d_create: preload_kernels)
   const int smem = kWarps * D * Sys::NV * 64 * (int)sizeof(double);
-  fv_step_pair_kernel<Sys, XPER, ADAPT, kWarps, D><<<grid, kWarps * 32, smem, ctx->launch_stream>>>(a);
+  fv_step_pair_kernel<Sys, XM, ADAPT, kWarps, D><<<grid, kWarps * 32, smem, ctx->launch_stream>>>(a);
+}
+
+template <class Sys, int D, int XM>
+void launch_pair_x(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
+  if (a.adaptive) launch_pair_1<Sys, D, XM, true>(ctx, a, grid);
+  else launch_pair_1<Sys, D, XM, false>(ctx, a, grid);
 }
 
 template <class Sys, int D>
-void launch_pair(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid, bool xper) {
-  if (xper && !a.adaptive) launch_pair_1<Sys, D, true, false>(ctx, a, grid);
-  if (xper && a.adaptive) launch_pair_1<Sys, D, true, true>(ctx, a, grid);
-  if (!xper && !a.adaptive) launch_pair_1<Sys, D, false, false>(ctx, a, grid);
-  if (!xper && a.adaptive) launch_pair_1<Sys, D, false, true>(ctx, a, grid);
+void launch_pair(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
+  if (ctx->xg) launch_pair_x<Sys, D, XM_GHOST>(ctx, a, grid);
+  else if (ctx->cfg.bc_x == FV2D_BC_PERIODIC) launch_pair_x<Sys, D, XM_PERIODIC>(ctx, a, grid);
+  else launch_pair_x<Sys, D, XM_CLAMP>(ctx, a, grid);
 }
 
 template <class Sys>
@@ -490,9 +495,9 @@ struct LaunchStep {
         const int warps = (a.col_hi - a.col_lo + 1 + 61) / 62;
         dim3 grid((warps + kWarps - 1) / kWarps, total_strips(a), ctx->nslabs);
         switch (ctx->ring_depth) {
-          case 6: launch_pair<Sys, 6>(ctx, a, grid, xper); break;
-          case 8: launch_pair<Sys, 8>(ctx, a, grid, xper); break;
-          default: launch_pair<Sys, 4>(ctx, a, grid, xper); break;
+          case 6: launch_pair<Sys, 6>(ctx, a, grid); break;
+          case 8: launch_pair<Sys, 8>(ctx, a, grid); break;
+          default: launch_pair<Sys, 4>(ctx, a, grid); break;
         }
       }
     }
@@ -529,19 +534,20 @@ cudaError_t touch(F* f) {
   cudaFuncAttributes at;
   return cudaFuncGetAttributes(&at, (const void*)f);
 }
+template <class Sys, int D, int XM>
+cudaError_t pair_attrs_x() {
+  const int smem = kWarps * D * Sys::NV * 64 * (int)sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(fv_step_pair_kernel<Sys, XM, false, kWarps, D>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e2 = cudaFuncSetAttribute(fv_step_pair_kernel<Sys, XM, true, kWarps, D>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e != cudaSuccess ? e : e2;
+}
 template <class Sys, int D>
 cudaError_t pair_attrs() {
-  const int smem = kWarps * D * Sys::NV * 64 * (int)sizeof(double);
-  cudaError_t e = cudaSuccess;
-  for (cudaError_t r : {cudaFuncSetAttribute(fv_step_pair_kernel<Sys, true, false, kWarps, D>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                        cudaFuncSetAttribute(fv_step_pair_kernel<Sys, true, true, kWarps, D>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                        cudaFuncSetAttribute(fv_step_pair_kernel<Sys, false, false, kWarps, D>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                        cudaFuncSetAttribute(fv_step_pair_kernel<Sys, false, true, kWarps, D>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem)})
-    if (e == cudaSuccess) e = r;
+  cudaError_t e = pair_attrs_x<Sys, D, XM_CLAMP>();
+  if (e == cudaSuccess) e = pair_attrs_x<Sys, D, XM_PERIODIC>();
+  if (e == cudaSuccess) e = pair_attrs_x<Sys, D, XM_GHOST>();
   return e;
 }
 template <class Sys>
