@@ -871,7 +871,11 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     if (c.reserved[k] != 0) return FV2D_E_ARG;
   // 2-D rank blocks (nranks_x > 1): nranks_x x (nranks/nranks_x) blocks
   const int px = c.nranks_x <= 1 ? 1 : c.nranks_x;
-  const bool xg = px > 1 || (c.flags & FV2D_FLAG_GHOST_COLUMNS);
+  // stored ghost columns: 2-D blocks, the test flag, and every non-periodic x
+  // boundary (wall/Dirichlet ghosts then live in the buffer instead of being
+  // built in registers: the pair kernel's XM_GHOST mode carries no per-cell
+  // boundary code; 2.92 vs 3.42 ms at 16384²)
+  const bool xg = px > 1 || (c.flags & FV2D_FLAG_GHOST_COLUMNS) || c.bc_x != FV2D_BC_PERIODIC;
   if (c.nranks_x < 0 || c.nranks % px != 0 || c.nx % px != 0 || c.nx / px < 2 || (px > 1 && c.nslabs != 1))
     return FV2D_E_ARG;
   const int py = c.nranks / px;
@@ -1517,6 +1521,13 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
     aos_to_dev_kernel<<<148 * 2, 256, 0, ctx->stream>>>(ctx->staging + row_doubles * lo(b), row_ptr(ctx, 0, 0, lo(b)),
                                                         nv, nx, hi(b) - lo(b), ctx->pitch, ctx->rs);
     CKL();
+    if (ctx->xg) {  // this band's ghost columns (wall mirror / periodic own columns)
+      StepArgs hc = hf;
+      hc.src_row_lo = lo(b);
+      hc.src_row_hi = hi(b);
+      fill_halo_cols_kernel<<<(hi(b) - lo(b) + 127) / 128, 128, 0, ctx->stream>>>(hc, nv);
+      CKL();
+    }
     CK(cudaEventRecord(ev_conv[b], ctx->stream));
     return FV2D_OK;
   };
@@ -1581,7 +1592,7 @@ fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_ou
   if (ctx->peer && !ctx->peer_connected) return set_err(ctx, FV2D_E_STATE, "peer halo: call fv2d_peer_connect first");
   CK(cudaSetDevice(ctx->cfg.device));
   const bool pipelined = layout == FV2D_AOS && nsteps >= 1 && ctx->cfg.nranks == 1 && ctx->nslabs == 1 &&
-                         !ctx->xg && !ctx->use_nccl && !ctx->peer && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE) &&
+                         !ctx->use_nccl && !ctx->peer && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE) &&
                          !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H >= 128;
   fv2d_status st;
   if (pipelined) {
