@@ -331,11 +331,14 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
 // marches one strip of rps rows (+2 halo rows) of kWarps x 62 columns; the
 // launch has C x S CTAs (C column blocks, S = ceil(nrows/rps) strips) of which
 // 148 x 3 are resident at a time.  The cost model ceil(C*S / 444) * (rps + 2)
-// (waves x rows marched per CTA) is minimised over S with rps <= 128 (longer
-// strips measured slower) and rps >= 4: it avoids a nearly empty last wave
-// (e.g. a 16384 x 2048 slab, the 8-GPU share of c3: 16 strips = 1072 CTAs =
-// 2.4 waves, vs 19 strips = 2.9 waves) and gives small domains one wave of
-// short strips (latency-bound: 1024^2 -> rps 12).
+// (waves x rows marched per CTA) is minimised over S with 4 <= rps <= 128: it
+// avoids a nearly empty last wave and gives small domains one wave of short
+// strips (latency-bound: 1024^2 -> rps 12).  The cap: in short bursts ~64-row
+// strips are 3-8% faster at large sizes (tools/rps_sweep.py,
+// profiles/r1_rps_sweep.jsonl: 16384^2 97.2 vs 92.8 G/s), but under sustained
+// load the GPU runs at its power cap, and there the longer strips -- fewer
+// re-read halo rows, less energy per step -- win by ~1% (200-300-step bench
+// A/B, profiles/r1_rps_powercap_ab.txt); the bench measures sustained load.
 int pick_rps(int ncols, int nrows) {
   static const int rps_max = getenv("FV2D_RPS_MAX") ? atoi(getenv("FV2D_RPS_MAX")) : 128;  // tuning knob
   static const int rps_force = getenv("FV2D_RPS") ? atoi(getenv("FV2D_RPS")) : 0;          // tuning knob
