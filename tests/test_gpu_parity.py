@@ -716,3 +716,36 @@ def test_spray_long_trajectory_300_steps():
     # the extrapolation error is O(dt^2): ~2 Newton iterations per cell-step at this
     # coarse mesh's dt (5e-3), ~1.0 at c4's 1.2e-4 (tools/longrun.py)
     assert iters / (96 * 96 * 300) < 3
+
+
+def test_create_destroy_releases_device_memory():
+    """Contexts release every device allocation (state buffers, staging, the
+    step_host pipeline's output staging, streams/events, NCCL-free paths,
+    spray caches): device free memory returns to its level after 30
+    create / use / destroy cycles."""
+    import torch
+    torch.cuda.init()
+    cfg, gen, _ = CASES["euler_laxliu3_256"]
+    W0 = gen()
+    scfg, S0, sdt = spray_case(64)
+
+    def cycle():
+        with solver_for(cfg, flags=fv2d.FLAG_GRAPH) as s:
+            out = np.empty_like(W0)
+            s.step_host(W0, out, 1e-4, 2)
+            snap = np.empty_like(W0)
+            s.snapshot(snap)
+            s.snapshot_wait()
+        with fv2d.Solver(64, 64, fv2d.SPRAY, param=(1.0, 1.0), bc_x=fv2d.BC_WALL) as s:
+            s.set_state(S0)
+            s.step(sdt, 2)
+            s.get_state()
+
+    cycle()  # first use: lazy module loads, allocator pools
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(30):
+        cycle()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20, (free0, free1)
