@@ -102,3 +102,26 @@ def test_c_client_runs():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "c_client ok" in r.stdout
+
+
+def test_struct_layouts_match_the_c_header(tmp_path):
+    """The ctypes mirrors of fv2d_config / fv2d_stats have the C header's size
+    and field offsets (compiled and measured with gcc)."""
+    src = tmp_path / "layout.c"
+    cfg_fields = [f for f, _ in fv2d.Config._fields_]
+    st_fields = [f for f, _ in fv2d.Stats._fields_]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "fv2d.h"', "int main(void) {",
+             'printf("%zu %zu\\n", sizeof(fv2d_config), sizeof(fv2d_stats));']
+    lines += [f'printf("%zu\\n", offsetof(fv2d_config, {f}));' for f in cfg_fields]
+    lines += [f'printf("%zu\\n", offsetof(fv2d_stats, {f}));' for f in st_fields]
+    lines += ["return 0; }"]
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    r = subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()
+    sizes, offs = out[:2], [int(x) for x in out[2:]]
+    assert int(sizes[0]) == C.sizeof(fv2d.Config) and int(sizes[1]) == C.sizeof(fv2d.Stats)
+    got = [getattr(fv2d.Config, f).offset for f in cfg_fields] + [getattr(fv2d.Stats, f).offset for f in st_fields]
+    assert offs == got
