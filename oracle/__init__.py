@@ -28,7 +28,11 @@ NVAR = {ADVECTION: 1, EULER: 4, SPRAY: 6}
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle (gcc, strict IEEE: no FMA contraction, no fast-math)."""
+    """Compile the oracle (gcc, strict IEEE: no FMA contraction, no fast-math).
+    ``FV2D_ORACLE_LIB`` names a prebuilt oracle instead (tools/mutate_oracle.py
+    points it at deliberately broken builds to show that the pins catch them)."""
+    if os.environ.get("FV2D_ORACLE_LIB"):
+        return os.environ["FV2D_ORACLE_LIB"]
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
@@ -68,6 +72,7 @@ def _L():
         _lib.or_reconstruct.argtypes = [d, d, d, d, P(C.c_int32)]
         _lib.or_gl24.argtypes = [d, d]
         _lib.or_gl24.restype = None
+        _lib.or_spray_guard.argtypes = [cfg, d, C.c_double, err]
         _lib.or_run.argtypes = [cfg, d, C.c_int32, C.c_int32, C.c_double, d, P(C.c_int32),
                                 C.c_int32, d, P(C.c_int32), P(C.c_int64), err]
     return _lib
@@ -194,6 +199,14 @@ def reconstruct(m):
     rc = _L().or_reconstruct(_dp(m), _dp(lam), _dp(n0), _dp(mmh), C.byref(it))
     _check(rc)
     return lam, float(n0[0]), float(mmh[0]), int(it.value)
+
+
+def spray_guard(cfg: Config, W, dt: float):
+    """S:440 startup guard: raises OracleError(E_ARG, argmin cell, min m3/m1)
+    when dt*K > 0.1*min(m3/m1)."""
+    W = _aos(cfg, W)
+    e = _Err()
+    _check(_L().or_spray_guard(C.byref(cfg._c()), _dp(W), dt, C.byref(e)), e)
 
 
 def gl24():

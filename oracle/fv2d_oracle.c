@@ -27,6 +27,12 @@
  *   or_reconstruct              pinned (uniform NDF, closed-form lambda=(0,1,0,0))
  *   or_source_step              pinned (uniform NDF closed form, drag-only ODE)
  *   or_gl24                     pinned (polynomial exactness to degree 47)
+ *   or_spray_guard              pinned (closed-form boundary dt = 0.1*min(m3/m1)/K)
+ *   ghosts (get_state)          pinned (Dirichlet: exact rationals, 50-digit,
+ *                               constant-state; wall: closed forms, 50-digit,
+ *                               conservation) -- tests/test_oracle_boundaries.py
+ *   spray phys_flux / speed     pinned (uniform velocity == per-moment upwind
+ *                               bitwise; 50-digit primitive-notation step)
  */
 #include <math.h>
 #include <stdint.h>
@@ -437,12 +443,35 @@ int or_source_step(const or_cfg* c, double* W, double dt, int64_t* iters_sum, or
   return OR_OK;
 }
 
+/* Source-step realizability guard (SPEC "Design decisions"): reject
+ * a run whose first dt has dt*K > 0.1*min_cells(m3/m1), erroring at startup
+ * (forward Euler, eq:SourceTerm, could destroy positivity).  CEO:
+ * r = m3/m1 per cell, rmin by `<` (lowest index on ties), reject iff
+ * (dt*K) > (0.1*rmin).  Returns OR_E_ARG with the argmin cell and rmin.     */
+int or_spray_guard(const or_cfg* c, const double* W, double dt, or_err* err) {
+  if (c->system != OR_SPRAY) return OR_OK;
+  const double K = c->param[0];
+  double rmin = INFINITY;
+  int64_t arg = -1;
+  for (size_t n = 0; n < (size_t)c->nx * c->ny; ++n) {
+    const double r = W[n * 6 + 3] / W[n * 6 + 1];
+    if (r < rmin) { rmin = r; arg = (int64_t)n; }
+  }
+  if ((dt * K) > (0.1 * rmin)) {
+    if (err) { err->code = OR_E_ARG; err->cell = arg; err->value = rmin; }
+    return OR_E_ARG;
+  }
+  return OR_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Full time loop (DESIGN.md §3.1 steps 1-8).
  *   mode 0 = fixed dt (value = dt): check dt*smax <= min(dx,dy) at the
  *            beginning of every iteration (R14); on violation the
  *            state is left at W^k and OR_E_CFL is returned.
  *   mode 1 = adaptive: dt_n = (value*hmin)/smax(W^n), value = C (R4/R5).
+ * Spray: the first step's dt must pass or_spray_guard, else OR_E_ARG
+ * with W untouched.
  * W (AoS) is advanced in place by nsteps.  dt_log (nsteps, may be NULL)
  * receives every dt used.  dump_steps (sorted, ndump) / dumps: W^k copies
  * for k in dump_steps (k = 0 means the input).  steps_done: completed steps. */
@@ -475,6 +504,10 @@ int or_run(const or_cfg* c, double* W, int32_t nsteps, int32_t mode, double valu
       }
     } else {
       dt = (value * hmin) / smax;
+    }
+    if (s == 0 && c->system == OR_SPRAY) {
+      rc = or_spray_guard(c, W, dt, err);
+      if (rc) break;
     }
     if (dt_log) dt_log[s] = dt;
     rc = or_transport_step(c, W, tmp, dt, err);

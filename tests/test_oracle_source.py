@@ -166,3 +166,127 @@ def test_spray_run_stays_realizable():
         W = O.run(cfg, W, 1, O.FIXED, dt).W
         assert _realizable(W)
     assert W[..., 0].sum() < W0[..., 0].sum()   # evaporation removes droplets
+
+
+def test_spray_guard_closed_form_boundary():
+    """S:440 (SPEC "Design decisions"): reject a run whose dt has
+    dt*K > 0.1*min over cells of m3/m1, erroring at startup with the state
+    untouched.  Uniform moments with m3/m1 = 1/2 and K = 1 put the boundary at
+    dt = 0.1*0.5 = 0.05 (0.1*0.5 is fl(0.1)/2 = fl(0.05): halving is exact):
+    dt = 0.05 runs, the next double above is rejected; the argmin cell is the
+    lowest-index cell with the smallest ratio."""
+    n = 4
+    cfg = _spray_cfg(n)
+    st = [0.75, 0.5, 0.375, 0.25, 0.0, 0.0]
+    W = inputs.uniform(n, n, st)
+    O.spray_guard(cfg, W, 0.05)
+    with pytest.raises(O.OracleError) as e:
+        O.spray_guard(cfg, W, np.nextafter(0.05, 1.0))
+    assert e.value.code == O.E_ARG and e.value.value == 0.5 and e.value.cell == 0
+    W2 = W.copy()
+    W2[2, 1, 3] = 0.125          # m3/m1 = 1/4 at cell (i=1, j=2): boundary dt = 0.025
+    W2[3, 2, 3] = 0.125
+    with pytest.raises(O.OracleError) as e:
+        O.spray_guard(cfg, W2, 0.03)
+    assert e.value.cell == 2 * n + 1 and e.value.value == 0.25
+    # through the time loop: E_ARG at startup, W^0 returned, no step taken
+    res = O.run(cfg, W2, 3, O.FIXED, 0.03, raise_on_error=False)
+    assert res.status == O.E_ARG and res.steps_done == 0 and np.array_equal(res.W, W2)
+    # K scales the boundary: K = 2 halves it
+    cfg2 = _spray_cfg(n, K=2.0)
+    O.spray_guard(cfg2, W, 0.025)
+    with pytest.raises(O.OracleError):
+        O.spray_guard(cfg2, W, 0.026)
+
+
+def test_spray_guard_adaptive_first_dt_and_r16_ic():
+    """The guard applies to the first dt of an adaptive run too; the R16 IC at
+    64^2 with the paper's fixed dt passes it (7.8e-3 <= 5.0e-2)."""
+    n = 64
+    W0 = inputs.spray_taylor_green(n, n)
+    cfg = _spray_cfg(n)
+    s0, _ = O.smax(cfg, W0)
+    dt = 0.5 * (1.0 / n) / s0
+    rmin = float(np.min(W0[..., 3] / W0[..., 1]))
+    assert dt * 1.0 <= 0.1 * rmin
+    O.run(cfg, W0, 1, O.FIXED, dt)
+    big_k = _spray_cfg(n, K=0.2 * rmin / dt)      # dt*K = 2 * 0.1 rmin
+    res = O.run(big_k, W0, 2, O.ADAPTIVE, 0.5, raise_on_error=False)
+    assert res.status == O.E_ARG and res.steps_done == 0
+
+
+def _decimal_newton_iterations(m):
+    """S:401-409 + R19 in 40-digit decimal, step by step: lambda = (-ln m0, 0, 0, 0);
+    mu_j = 2 sum_q w_q t_q^j exp(-P(t_q)) on GL-24 mapped to [0,1] (numpy
+    leggauss nodes); while max_k |mu_{k+1} - m_k|/m_k > 1e-10: solve
+    H d = mu_{1..4} - m (H_kl = mu_{k+l+1}, Gaussian elimination), backtrack
+    alpha = 1, 1/2, ... until the residual decreases.  Returns the count."""
+    from decimal import Decimal as D, getcontext
+    getcontext().prec = 40
+    xg, wg = np.polynomial.legendre.leggauss(24)
+    t = [(D(float(x)) + 1) / 2 for x in xg]
+    w = [D(float(x)) / 2 for x in wg]
+    md = [D(float(x)) for x in m]
+
+    def mom(lam):
+        mu = [D(0)] * 8
+        for q in range(24):
+            e = (-(lam[0] + t[q] * (lam[1] + t[q] * (lam[2] + t[q] * lam[3])))).exp()
+            for j in range(8):
+                mu[j] += 2 * w[q] * t[q] ** j * e
+        return mu
+
+    def res(mu):
+        return max(abs(mu[k + 1] - md[k]) / md[k] for k in range(4))
+
+    lam = [-md[0].ln(), D(0), D(0), D(0)]
+    mu = mom(lam)
+    r0 = res(mu)
+    it = 0
+    while r0 > D("1e-10"):
+        A = [[mu[k + l + 1] for l in range(4)] + [mu[k + 1] - md[k]] for k in range(4)]
+        for c in range(4):
+            for r in range(c + 1, 4):
+                f = A[r][c] / A[c][c]
+                A[r] = [A[r][k] - f * A[c][k] for k in range(5)]
+        d = [D(0)] * 4
+        for c in range(3, -1, -1):
+            d[c] = (A[c][4] - sum(A[c][k] * d[k] for k in range(c + 1, 4))) / A[c][c]
+        a = D(1)
+        for _ in range(31):
+            lt = [lam[k] + a * d[k] for k in range(4)]
+            mt = mom(lt)
+            rt = res(mt)
+            if rt < r0:
+                lam, mu, r0 = lt, mt, rt
+                break
+            a /= 2
+        it += 1
+        assert it <= 50
+    return it
+
+
+def test_newton_iteration_counts_match_decimal_algorithm():
+    """S:405's stopping rule (max relative moment residual <= 1e-10, residual of
+    moment k relative to m_k) and the backtracking of R19: on 50 random
+    realizable sets (SURVEY A6 distribution) the oracle takes exactly as many
+    Newton iterations as the same algorithm run in 40-digit decimal."""
+    rng = np.random.default_rng(2024)
+    for _ in range(50):
+        lam_true = np.array([rng.uniform(-1, 1), rng.uniform(-2, 2), rng.uniform(-2, 2), rng.uniform(-1, 1)])
+        mm = _quad_moments(lam_true)
+        assert O.reconstruct(mm[1:])[3] == _decimal_newton_iterations(mm[1:])
+
+
+def test_polished_reconstruction_reaches_the_root():
+    """R19: after convergence one undamped Newton step polishes lambda, so
+    (n(0), m_-1/2) reach the GL-24 root to conditioning x rounding -- within
+    1e-11 (n0) and 1e-12 (m_-1/2) of the true values exp(-lambda0_true) and the
+    adaptive-quadrature m_-1/2 (stopping at 1e-10 alone leaves up to ~5e-9)."""
+    rng = np.random.default_rng(2024)
+    for _ in range(50):
+        lam_true = np.array([rng.uniform(-1, 1), rng.uniform(-2, 2), rng.uniform(-2, 2), rng.uniform(-1, 1)])
+        mm = _quad_moments(lam_true)
+        lam, n0, mmh, _ = O.reconstruct(mm[1:])
+        assert n0 == pytest.approx(math.exp(-lam_true[0]), rel=1e-11, abs=0)
+        assert mmh == pytest.approx(mm[0], rel=1e-12, abs=0)
