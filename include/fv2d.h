@@ -147,6 +147,11 @@ typedef struct {
   double source_kernel_ms;    /* with profiling on: summed device time of the split spray
                                  source kernels of steps (not captured in a CUDA graph) */
   int64_t source_kernels_timed;
+  int32_t sms;             /* multiprocessors of the context's device */
+  int32_t resident_ctas;   /* resident CTAs of the marching step kernel (SMs x occupancy API),
+                              the launch-shape cost model's wave size */
+  int32_t strip_rows;      /* rows per CTA strip chosen for a full-slab launch */
+  int32_t reserved0;
 } fv2d_stats;
 
 /* Library version; never fails. */

@@ -192,6 +192,10 @@ struct fv2d_ctx {
   // host state
   bool has_state = false;
   bool dt_valid = false;
+  double dt_cfl = 0.0;       // the C that dt_dev was computed with (adaptive mode)
+  int sms = 0;               // multiprocessors of cfg.device
+  int slots = 0;             // resident CTAs of the marching step kernel (sms x occupancy)
+  bool guard_done = false;   // S:440 guard passed since the last set_state
   long long steps = 0;
   long long launches = 0;
   // profiling: event pairs around step-kernel launches
@@ -330,7 +334,9 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
 // Strip height of a marching-kernel launch over ncols x nrows cells.  A CTA
 // marches one strip of rps rows (+2 halo rows) of kWarps x 62 columns; the
 // launch has C x S CTAs (C column blocks, S = ceil(nrows/rps) strips) of which
-// 148 x 3 are resident at a time.  The cost model ceil(C*S / 444) * (rps + 2)
+// `slots` = SMs x resident CTAs per SM are resident at a time (queried at
+// fv2d_create from the device and the occupancy API for the kernel the context
+// launches: 148 x 3 = 444 for the B200 pair kernel).  The cost model ceil(C*S / slots) * (rps + 2)
 // (waves x rows marched per CTA) is minimised over S with 4 <= rps <= 128: it
 // avoids a nearly empty last wave and gives small domains one wave of short
 // strips (latency-bound: 1024^2 -> rps 12).  The cap: in short bursts ~64-row
@@ -339,12 +345,14 @@ void ghost_targets(const fv2d_ctx* ctx, int s, int q, SlabDesc& d) {
 // load the GPU runs at its power cap, and there the longer strips -- fewer
 // re-read halo rows, less energy per step -- win by ~1% (200-300-step bench
 // A/B, profiles/r1_rps_powercap_ab.txt); the bench measures sustained load.
-int pick_rps(int ncols, int nrows) {
+int num_sms(const fv2d_ctx* ctx) { return ctx->sms > 0 ? ctx->sms : 148; }
+
+int pick_rps(const fv2d_ctx* ctx, int ncols, int nrows) {
   static const int rps_max = getenv("FV2D_RPS_MAX") ? atoi(getenv("FV2D_RPS_MAX")) : 128;  // tuning knob
   static const int rps_force = getenv("FV2D_RPS") ? atoi(getenv("FV2D_RPS")) : 0;          // tuning knob
   if (rps_force > 0) return std::min(rps_force, std::max(1, nrows));
   const long long C = ((ncols + 62) / 62 + kWarps - 1) / kWarps;
-  const long long slots = 148LL * 3;
+  const long long slots = std::max(1, ctx->slots);
   const int s_min = std::max(1, (nrows + rps_max - 1) / rps_max);
   const int s_max = std::max(s_min, nrows / 4);
   long long best_cost = -1;
@@ -511,7 +519,7 @@ template <class Sys>
 struct LaunchReduce {
   static void run(const fv2d_ctx* ctx, const StepArgs& a) {
     const long long n = (long long)ctx->nx * ctx->H;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+    int blocks = (int)std::min<long long>((n + 255) / 256, num_sms(ctx) * 8);
     reduce_smax_kernel<Sys><<<dim3(blocks, 1, ctx->nslabs), 256, 0, ctx->stream>>>(a);
   }
 };
@@ -520,10 +528,63 @@ template <class Sys>
 struct LaunchArgmax {
   static void run(const fv2d_ctx* ctx, const StepArgs& a, double smax, unsigned long long* out) {
     const long long n = (long long)ctx->nx * ctx->H;
-    int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+    int blocks = (int)std::min<long long>((n + 255) / 256, num_sms(ctx) * 8);
     argmax_kernel<Sys><<<dim3(blocks, 1, ctx->nslabs), 256, 0, ctx->stream>>>(a, smax, out);
   }
 };
+
+// Device geometry for the launch-shape cost models: SM count and the resident
+// CTAs per SM of the marching kernel this context launches (fixed-dt
+// instantiation), from the occupancy API -- so a register-budget change or
+// another GPU re-tunes the strip height instead of silently mis-tuning it.
+template <class Sys>
+struct Occupancy {
+  static cudaError_t run(const fv2d_ctx* ctx, int* per_sm) {
+    constexpr int D = 4;
+    const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC && !ctx->xg;
+    if constexpr (Sys::NV == 6) {  // the one-cell kernel (LaunchStep)
+      if (!(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE))
+        return xper ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, true, false, kWarps, D, false>, kWarps * 32, 0)
+                    : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, false, false, kWarps, D, false>, kWarps * 32, 0);
+      return xper ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, true, false, kWarps, D>, kWarps * 32, 0)
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, false, false, kWarps, D>, kWarps * 32, 0);
+    } else {
+    if (ctx->cfg.flags & FV2D_FLAG_ONE_CELL)
+      return xper ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, true, false, kWarps, D>, kWarps * 32, 0)
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, false, false, kWarps, D>, kWarps * 32, 0);
+    const int Dr = ctx->ring_depth == 6 || ctx->ring_depth == 8 ? ctx->ring_depth : 4;
+    const size_t smem = (size_t)kWarps * Dr * Sys::NV * 64 * sizeof(double);
+    auto occ = [&](auto kern) { return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, kWarps * 32, smem); };
+    if (Dr == 4) {
+      if (ctx->xg) return occ(fv_step_pair_kernel<Sys, XM_GHOST, false, kWarps, 4>);
+      if (xper) return occ(fv_step_pair_kernel<Sys, XM_PERIODIC, false, kWarps, 4>);
+      return occ(fv_step_pair_kernel<Sys, XM_CLAMP, false, kWarps, 4>);
+    }
+    if (Dr == 6) {
+      if (ctx->xg) return occ(fv_step_pair_kernel<Sys, XM_GHOST, false, kWarps, 6>);
+      if (xper) return occ(fv_step_pair_kernel<Sys, XM_PERIODIC, false, kWarps, 6>);
+      return occ(fv_step_pair_kernel<Sys, XM_CLAMP, false, kWarps, 6>);
+    }
+    if (ctx->xg) return occ(fv_step_pair_kernel<Sys, XM_GHOST, false, kWarps, 8>);
+    if (xper) return occ(fv_step_pair_kernel<Sys, XM_PERIODIC, false, kWarps, 8>);
+    return occ(fv_step_pair_kernel<Sys, XM_CLAMP, false, kWarps, 8>);
+    }
+  }
+};
+
+cudaError_t query_geometry(fv2d_ctx* ctx) {
+  cudaError_t e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  switch (ctx->cfg.system) {
+    case FV2D_ADVECTION: e = Occupancy<Advection>::run(ctx, &per_sm); break;
+    case FV2D_EULER: e = Occupancy<Euler>::run(ctx, &per_sm); break;
+    default: e = Occupancy<Spray>::run(ctx, &per_sm); break;
+  }
+  if (e != cudaSuccess) return e;
+  ctx->slots = ctx->sms * std::max(1, per_sm);
+  return cudaSuccess;
+}
 
 // Load every kernel a context can launch, and set the pair kernels' dynamic
 // shared-memory opt-in, once per process and system at fv2d_create -- never
@@ -864,9 +925,11 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   const int nv = nvar_of(c.system);
   if (nv < 0 || c.nvar != nv || c.nx < 1 || c.ny < 1 || c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks ||
       c.nslabs < 1 || c.nslabs > kMaxSlabs || ((c.nranks > 1 || (c.flags & FV2D_FLAG_NCCL_LOOPBACK)) && c.nslabs != 1) ||
-      c.ny % ((c.nranks_x > 1 ? c.nranks / c.nranks_x : c.nranks) * c.nslabs) != 0 || !(c.x1 > c.x0) || !(c.y1 > c.y0) || c.bc_x < 0 || c.bc_x > 2 ||
-      c.bc_y < 0 || c.bc_y > 2)
+      !(c.x1 > c.x0) || !(c.y1 > c.y0) || c.bc_x < 0 || c.bc_x > 2 || c.bc_y < 0 || c.bc_y > 2)
     return FV2D_E_ARG;
+  // the rank grid before any division by it: 0 <= nranks_x <= nranks, nranks % nranks_x == 0
+  if (c.nranks_x < 0 || c.nranks_x > c.nranks || (c.nranks_x > 1 && c.nranks % c.nranks_x != 0)) return FV2D_E_ARG;
+  if (c.ny % ((c.nranks_x > 1 ? c.nranks / c.nranks_x : c.nranks) * c.nslabs) != 0) return FV2D_E_ARG;
   if (c.system == FV2D_ADVECTION && (c.bc_x == FV2D_BC_WALL || c.bc_y == FV2D_BC_WALL)) return FV2D_E_ARG;
   if (c.system == FV2D_EULER && !(c.param[0] > 1.0)) return FV2D_E_ARG;
   if (c.system == FV2D_SPRAY && !(c.param[1] > 0.0)) return FV2D_E_ARG;
@@ -915,7 +978,6 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   ctx->pitch = (nxl + ctx->xoff + (xg ? 1 : 0) + 31) / 32 * 32;
   if (const char* e = getenv("FV2D_RING_DEPTH")) ctx->ring_depth = atoi(e);  // tuning knob
   ctx->rs = (long long)ctx->pitch * nv;
-  ctx->rps = pick_rps(nxl, (int)H);
   ctx->nslabs = c.nslabs;
   ctx->G = py * c.nslabs;
   ctx->dx = (c.x1 - c.x0) / c.nx;
@@ -962,6 +1024,8 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     }
   }
   CKC(preload_kernels(c.system, c.device));
+  CKC(query_geometry(ctx));
+  ctx->rps = pick_rps(ctx, nxl, (int)H);
   if (peer) {
     CKC(cudaMalloc(&ctx->sync, sizeof(PeerSync)));
     CKC(cudaMemset(ctx->sync, 0, sizeof(PeerSync)));
@@ -985,13 +1049,20 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     trig_table_kernel<<<(c.ny + 255) / 256, 256>>>(ctx->trig + 2 * c.nx, ctx->trig + 2 * c.nx + c.ny, c.ny, c.y0,
                                                     ctx->dy);
     CKC(cudaGetLastError());
-    static bool gl_done = false;
-    if (!gl_done) {
-      double t[24], wt[24][8];
-      gl24_table(t, wt);
-      CKC(cudaMemcpyToSymbol(c_gl_t, t, sizeof t));
-      CKC(cudaMemcpyToSymbol(c_gl_wt, wt, sizeof wt));
-      gl_done = true;
+    // __constant__ symbols exist once per device: upload the table to every
+    // device a spray context is created on (under the preload mutex: contexts
+    // may be created from several threads)
+    {
+      static std::mutex gl_mu;
+      static std::set<int> gl_devices;
+      std::lock_guard<std::mutex> lk(gl_mu);
+      if (!gl_devices.count(c.device)) {
+        double t[24], wt[24][8];
+        gl24_table(t, wt);
+        CKC(cudaMemcpyToSymbol(c_gl_t, t, sizeof t));
+        CKC(cudaMemcpyToSymbol(c_gl_wt, wt, sizeof wt));
+        gl_devices.insert(c.device);
+      }
     }
   }
   // Dirichlet ghost rows are constant for the whole run.
@@ -1062,6 +1133,7 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->has_state = true;
   ctx->dt_valid = false;
+  ctx->guard_done = false;
   ctx->lam_hist = 0;
   ctx->err.clear();
   ctx->err_step = ctx->err_cell = -1;
@@ -1099,7 +1171,7 @@ static fv2d_status upload(fv2d_ctx* ctx, const double* src, fv2d_layout layout, 
     const size_t bytes = (size_t)nv * nx * H * ctx->nslabs * sizeof(double);
     CK(cudaMemcpyAsync(ctx->staging, src, bytes, kind, ctx->stream));
     for (int s = 0; s < ctx->nslabs; ++s) {
-      aos_to_dev_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->staging + (size_t)s * H * nx * nv,
+      aos_to_dev_kernel<<<num_sms(ctx) * 8, 256, 0, ctx->stream>>>(ctx->staging + (size_t)s * H * nx * nv,
                                                           row_ptr(ctx, s, 0, 0), nv, nx, H, ctx->pitch, ctx->rs);
       CKL();
     }
@@ -1139,7 +1211,7 @@ fv2d_status fv2d_get_state(fv2d_ctx* ctx, double* host, fv2d_layout layout) {
     fv2d_status s1 = ensure_staging(ctx);
     if (s1) return s1;
     for (int s = 0; s < ctx->nslabs; ++s) {
-      dev_to_aos_kernel<<<148 * 8, 256, 0, ctx->stream>>>(row_ptr(ctx, s, p, 0),
+      dev_to_aos_kernel<<<num_sms(ctx) * 8, 256, 0, ctx->stream>>>(row_ptr(ctx, s, p, 0),
                                                           ctx->staging + (size_t)s * H * nx * nv, nv, nx, H,
                                                           ctx->pitch, ctx->rs);
       CKL();
@@ -1173,6 +1245,7 @@ fv2d_status fv2d_compute_dt(fv2d_ctx* ctx, double cfl, double* dt, double* smax)
   CK(cudaMemcpyAsync(ctx->dt_dev, &d, sizeof d, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->dt_valid = true;
+  ctx->dt_cfl = cfl;
   return FV2D_OK;
 }
 
@@ -1282,8 +1355,8 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
     if (ctx->xg) {  // column strips [0, cb) and [ce, nx) of the interior rows
       const int ce = (ctx->nx - cb) & ~1;
       StepArgs bw = at, be = at;
-      set_ranges(bw, hb, ctx->H - hb, pick_rps(cb, ctx->H - 2 * hb), 0, 0, 1);
-      set_ranges(be, hb, ctx->H - hb, pick_rps(ctx->nx - ce, ctx->H - 2 * hb), 0, 0, 1);
+      set_ranges(bw, hb, ctx->H - hb, pick_rps(ctx, cb, ctx->H - 2 * hb), 0, 0, 1);
+      set_ranges(be, hb, ctx->H - hb, pick_rps(ctx, ctx->nx - ce, ctx->H - 2 * hb), 0, 0, 1);
       bw.col_lo = 0;
       bw.col_hi = cb;
       be.col_lo = ce;
@@ -1322,7 +1395,7 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
         const int r_hi = (int)((long long)(ty + 1) * ctx->H / ctx->tiles_y);
         t.col_lo = (int)((long long)tx * ctx->nx / ctx->tiles_x) & ~1;
         t.col_hi = tx + 1 == ctx->tiles_x ? ctx->nx : (int)((long long)(tx + 1) * ctx->nx / ctx->tiles_x) & ~1;
-        set_ranges(t, r_lo, r_hi, pick_rps(t.col_hi - t.col_lo, r_hi - r_lo), 0, 0, 1);
+        set_ranges(t, r_lo, r_hi, pick_rps(ctx, t.col_hi - t.col_lo, r_hi - r_lo), 0, 0, 1);
         dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, t);
         CKL();
       }
@@ -1402,6 +1475,12 @@ static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double
 static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double cfl, int32_t nsteps) {
   fv2d_status st = ensure_dt_log(ctx, ctx->steps + nsteps);
   if (st) return st;
+  // dt_dev holds dt_{n} = (C*hmin)/smax(W^n) only after adaptive steps with
+  // this C: the fixed-dt finalize does not refresh it
+  if (nsteps > 0) {
+    ctx->dt_valid = adaptive != 0;
+    ctx->dt_cfl = cfl;
+  }
   const bool split = ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE);
   const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl && !ctx->peer;
   for (int32_t k = 0; k < nsteps; ++k) {
@@ -1435,10 +1514,69 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
   return FV2D_OK;
 }
 
+// S:440 startup guard of the spray (SPEC "Design decisions"), before the first
+// step after set_state, in the oracle's order (or_run): a
+// non-admissible W^0 and (fixed dt) a CFL violation take precedence -- the
+// step itself then latches them -- else reject dt*K > 0.1*min(m3/m1) with
+// FV2D_E_ARG and launch nothing.  Collective over the ranks (every rank calls
+// the first step after set_state); synchronous, once per set_state.
+static fv2d_status spray_guard(fv2d_ctx* ctx, double dt, bool fixed) {
+  if (ctx->cfg.system != FV2D_SPRAY || ctx->guard_done || ctx->steps != 0) return FV2D_OK;
+  unsigned long long st;
+  fv2d_status s0 = read_status(ctx, &st);
+  if (s0) return s0;
+  if (st) return FV2D_OK;  // latched error: the steps are no-ops and report it
+  if (fixed) {
+    double smax;
+    unsigned long long pend;
+    s0 = reduce_current(ctx, &smax, &pend);
+    if (s0) return s0;
+    if (pend || dt * smax > ctx->hmin) return FV2D_OK;  // the step latches E_NONFINITE / E_CFL
+  }
+  const StepArgs a = make_args(ctx, cur_parity(ctx));
+  const dim3 grid(num_sms(ctx) * 4, 1, ctx->nslabs);
+  CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  spray_guard_kernel<<<grid, 256, 0, ctx->stream>>>(a, ctx->dscal + 0, 0.0, nullptr);
+  CKL();
+  unsigned long long h = 0;
+  if (ctx->use_nccl || ctx->peer) {
+    s0 = reduce_ranks(ctx, ctx->stream);
+    if (s0) return s0;
+    CK(cudaMemcpyAsync(&h, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    CK(cudaMemcpyAsync(&h, ctx->dscal + 0, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double rmin = h ? min_key_decode(h) : INFINITY;
+  const double K = ctx->cfg.param[0];
+  if ((dt * K) > (0.1 * rmin)) {
+    CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
+    spray_guard_kernel<<<grid, 256, 0, ctx->stream>>>(a, nullptr, rmin, ctx->dscal + 3);
+    CKL();
+    unsigned long long cell = ~0ull;
+    CK(cudaMemcpyAsync(&cell, ctx->dscal + 3, sizeof cell, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->err_step = 0;
+    ctx->err_cell = cell == ~0ull ? -1 : (long long)cell;
+    ctx->err_value = rmin;
+    return set_err(ctx, FV2D_E_ARG,
+                   "S:440 guard: dt*K = %.17g > 0.1*min(m3/m1) = %.17g (cell %lld); no step taken", dt * K,
+                   0.1 * rmin, ctx->err_cell);
+  }
+  ctx->guard_done = true;
+  return FV2D_OK;
+}
+
 fv2d_status fv2d_step(fv2d_ctx* ctx, double dt, int32_t nsteps) {
   if (!ctx || !(dt > 0.0) || nsteps < 0 || !std::isfinite(dt)) return FV2D_E_ARG;
   if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
   CK(cudaSetDevice(ctx->cfg.device));
+  if (nsteps > 0) {
+    fv2d_status st = spray_guard(ctx, dt, true);
+    if (st) return st;
+  }
   return launch_steps(ctx, 0, dt, 0.0, nsteps);
 }
 
@@ -1446,10 +1584,15 @@ fv2d_status fv2d_step_adaptive(fv2d_ctx* ctx, double cfl, int32_t nsteps, double
   if (!ctx || !(cfl > 0.0) || !(cfl <= 1.0) || nsteps < 0) return FV2D_E_ARG;
   if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
   CK(cudaSetDevice(ctx->cfg.device));
-  if (!ctx->dt_valid) {
+  const bool guard = ctx->cfg.system == FV2D_SPRAY && !ctx->guard_done && ctx->steps == 0 && nsteps > 0;
+  if (!ctx->dt_valid || ctx->dt_cfl != cfl || guard) {
     double d, s;
     fv2d_status st = fv2d_compute_dt(ctx, cfl, &d, &s);
     if (st) return st;
+    if (guard) {
+      st = spray_guard(ctx, d, false);
+      if (st) return st;
+    }
   }
   const long long first = ctx->steps;
   fv2d_status st = launch_steps(ctx, 1, 0.0, cfl, nsteps);
@@ -1521,7 +1664,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   hf.slab[0].in = row_ptr(ctx, 0, 0, 0);
   auto convert_in = [&](int b) -> fv2d_status {
     CK(cudaStreamWaitEvent(ctx->stream, ev_in[b], 0));
-    aos_to_dev_kernel<<<148 * 2, 256, 0, ctx->stream>>>(ctx->staging + row_doubles * lo(b), row_ptr(ctx, 0, 0, lo(b)),
+    aos_to_dev_kernel<<<num_sms(ctx) * 2, 256, 0, ctx->stream>>>(ctx->staging + row_doubles * lo(b), row_ptr(ctx, 0, 0, lo(b)),
                                                         nv, nx, hi(b) - lo(b), ctx->pitch, ctx->rs);
     CKL();
     if (ctx->xg) {  // this band's ghost columns (wall mirror / periodic own columns)
@@ -1536,7 +1679,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   };
   auto step_band = [&](int b) -> fv2d_status {
     StepArgs t = at;
-    set_ranges(t, lo(b), hi(b), pick_rps(nx, hi(b) - lo(b)), 0, 0, 1);
+    set_ranges(t, lo(b), hi(b), pick_rps(ctx, nx, hi(b) - lo(b)), 0, 0, 1);
     dispatch<LaunchStep>(ctx->cfg.system, (const fv2d_ctx*)ctx, t);
     CKL();
     if (spray) {
@@ -1547,7 +1690,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
       spray_source_dt_kernel_launch(ctx, sb, grid, 0);
       CKL();
     }
-    dev_to_aos_kernel<<<148 * 2, 256, 0, ctx->stream>>>(row_ptr(ctx, 0, 1, lo(b)), ctx->staging_out + row_doubles * lo(b),
+    dev_to_aos_kernel<<<num_sms(ctx) * 2, 256, 0, ctx->stream>>>(row_ptr(ctx, 0, 1, lo(b)), ctx->staging_out + row_doubles * lo(b),
                                                         nv, nx, hi(b) - lo(b), ctx->pitch, ctx->rs);
     CKL();
     CK(cudaEventRecord(ev_out[b], ctx->stream));
@@ -1594,7 +1737,10 @@ fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_ou
     return FV2D_E_ARG;
   if (ctx->peer && !ctx->peer_connected) return set_err(ctx, FV2D_E_STATE, "peer halo: call fv2d_peer_connect first");
   CK(cudaSetDevice(ctx->cfg.device));
+  // the spray's first step needs all of W^0 on the device before it starts
+  // (the S:440 guard), so only transport systems pipeline the upload
   const bool pipelined = layout == FV2D_AOS && nsteps >= 1 && ctx->cfg.nranks == 1 && ctx->nslabs == 1 &&
+                         ctx->cfg.system != FV2D_SPRAY &&
                          !ctx->use_nccl && !ctx->peer && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE) &&
                          !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H >= 128;
   fv2d_status st;
@@ -1616,7 +1762,7 @@ fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_ou
   } else {
     st = fv2d_set_state(ctx, host_in, layout);
     if (st) return st;
-    st = launch_steps(ctx, 0, dt, 0.0, nsteps);
+    st = fv2d_step(ctx, dt, nsteps);
     if (st) return st;
   }
   return fv2d_get_state(ctx, host_out, layout);
@@ -1627,6 +1773,10 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
   if (ctx->cfg.system != FV2D_SPRAY) return FV2D_OK;  // S = 0
   CK(cudaSetDevice(ctx->cfg.device));
+  if (ctx->snap_parity >= 0) {  // in place: a snapshot may still be converting this buffer
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_snap_conv, 0));
+    ctx->snap_parity = -1;
+  }
   const int p = cur_parity(ctx);
   // in place on parity p: halo targets are the ghost buffers of parity p
   StepArgs b = make_args(ctx, 1 - p);
@@ -1731,7 +1881,7 @@ fv2d_status fv2d_snapshot(fv2d_ctx* ctx, double* host, fv2d_layout layout) {
   CK(cudaStreamWaitEvent(ctx->out_stream, ctx->ev_snap_start, 0));
   for (int s = 0; s < ctx->nslabs; ++s) {
     if (layout == FV2D_AOS) {
-      dev_to_aos_kernel<<<148 * 4, 256, 0, ctx->out_stream>>>(row_ptr(ctx, s, p, 0),
+      dev_to_aos_kernel<<<num_sms(ctx) * 4, 256, 0, ctx->out_stream>>>(row_ptr(ctx, s, p, 0),
                                                               ctx->snap_buf + (size_t)s * H * nx * nv, nv, nx, H,
                                                               ctx->pitch, ctx->rs);
       CKL();
@@ -1876,6 +2026,10 @@ fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out) {
   out->source_kernels_timed = ctx->prof_src_n;
   out->steps = ctx->steps;
   out->kernel_launches = ctx->launches;
+  out->sms = ctx->sms;
+  out->resident_ctas = ctx->slots;
+  out->strip_rows = ctx->rps;
+  out->reserved0 = 0;
   unsigned long long ni = 0;
   if (ctx->newton) cudaMemcpyAsync(&ni, ctx->newton, sizeof ni, cudaMemcpyDeviceToHost, ctx->stream);
   out->newton_iters = (int64_t)ni;

@@ -41,7 +41,9 @@ class Config(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("kernel_launches", C.c_int64), ("newton_iters", C.c_int64),
                 ("dt", C.c_double), ("step_kernel_ms", C.c_double), ("step_kernels_timed", C.c_int64),
-                ("source_kernel_ms", C.c_double), ("source_kernels_timed", C.c_int64)]
+                ("source_kernel_ms", C.c_double), ("source_kernels_timed", C.c_int64),
+                ("sms", C.c_int32), ("resident_ctas", C.c_int32), ("strip_rows", C.c_int32),
+                ("reserved0", C.c_int32)]
 
 
 _LIB = None
@@ -239,6 +241,8 @@ class Solver:
     def get_state(self, layout: int = AOS, out: np.ndarray | None = None, raise_on_error: bool = True):
         if out is None:
             out = np.empty(self._shape(layout))
+        elif out.shape != self._shape(layout) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError(f"get_state buffer must be float64 C-contiguous {self._shape(layout)}")
         rc = lib().fv2d_get_state(self._h, out.ctypes.data, layout)
         if raise_on_error:
             self._check(rc, "get_state")

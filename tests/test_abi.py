@@ -75,7 +75,9 @@ def test_create_validates_2d_rank_blocks():
                                          (4, 32, 4, 4, 1),    # 1-column blocks
                                          (64, 30, 8, 2, 1),   # 30 % (8/2)
                                          (64, 32, 4, 2, 2),   # slabs with blocks
-                                         (64, 32, 4, -1, 1)]:
+                                         (64, 32, 4, -1, 1),
+                                         (64, 32, 2, 4, 1),   # nranks_x > nranks (was a SIGFPE)
+                                         (64, 32, 1, 2, 1)]:  # nranks_x > nranks = 1
         L.fv2d_config_default(C.byref(cfg), nx, ny, fv2d.EULER)
         cfg.nranks, cfg.nranks_x, cfg.nslabs = nranks, px, nslabs
         cfg.flags = fv2d.FLAG_PEER_HALO
