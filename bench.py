@@ -77,57 +77,83 @@ def ncu_traffic(kernel_key):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """GPU clocks, power and clock-event (throttle) reasons, sampled in-process
+    through NVML every 10 ms from before the warm-up to the end of the run.
+    Each sample carries the phase label current when it was taken, so the
+    summary covers exactly the timed repetitions (or the sustained run)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.phase = "setup"
+        self.samples = []            # (phase, sm_mhz, reasons bitmask, power_w)
+        self.sm_max = None
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            # CUDA device index -> NVML index (NVML ignores CUDA_VISIBLE_DEVICES)
+            idx = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+            if vis and vis[0].strip() and self.device < len(vis) and vis[self.device].strip().isdigit():
+                idx = int(vis[self.device])
+            h = N.nvmlDeviceGetHandleByIndex(idx)
+            self._nvml, self._h = N, h
+            self.sm_max = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # no NVML: clocks stay unmeasured (reported as such)
+            self._err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N, h = self._nvml, self._h
+        while not self._stop.is_set():
+            try:
+                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                rs = int(N.nvmlDeviceGetCurrentClocksEventReasons(h))
+                pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.samples.append((self.phase, sm, rs, pw))
+            except Exception:
+                pass
+            self._stop.wait(0.01)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        self._stop.set()
+        if self._nvml is not None:
+            self._t.join(timeout=2)
             try:
-                self.proc.wait(timeout=5)
+                self._nvml.nvmlShutdown()
             except Exception:
-                self.proc.kill()
+                pass
 
-    def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+    def summary(self, phase="timed"):
+        rows = [x for x in self.samples if x[0] == phase]
+        reasons = sorted(n for n, bit in self.REASONS.items() if any(r & bit for _, _, r, _ in rows))
+        sm = [x[1] for x in rows]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.sm_max,
+                "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(rows),
+                "power_w_median": float(np.median([x[3] for x in rows])) if rows else None,
+                "source": "NVML in-process, 10 ms" if self._nvml is not None else
+                          f"unavailable ({getattr(self, '_err', '?')})"}
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cores": os.cpu_count(), "cpu_model": model}
 
 
 def gen_ic(system, nx, ny, rows):
@@ -174,7 +200,7 @@ def cpu_baseline(nx, ny, budget_s=12.0, system="euler"):
     from paper_1701_05431_b200 import inputs
     if system == "spray":
         v, n, el = spray_band_oracle(nx, ny, 8, budget_s)
-        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", **host_info(),
                 "sample": f"{n} spray steps (transport + source, cold-start Newton) on a {nx}x8 full-width row "
                           f"band of the workload, {el:.1f} s, 1 thread"}
     rows = min(ny, 256)
@@ -190,7 +216,7 @@ def cpu_baseline(nx, ny, budget_s=12.0, system="euler"):
         if time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
-    return {"value": nx * rows * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": nx * rows * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle", **host_info(),
             "sample": f"{steps} transport steps on a {nx}x{rows} full-width row band of the workload "
                       f"(periodic band), {el:.1f} s, 1 thread"}
 
@@ -213,7 +239,8 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": args.workload, "description": desc, "nx": nx, "ny": ny,
                                             "sample_rows": 2},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             **host_info()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
         return
@@ -238,9 +265,15 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "description": desc, "nx": nx, "ny": ny,
                                         "sample_rows": rows},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             **host_info()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def sha_state(W):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(W).tobytes()).hexdigest()
 
 
 def main():
@@ -261,6 +294,13 @@ def main():
     ap.add_argument("--nranks-x", type=int, default=1,
                     help="N>1: the ranks as a PX x (N/PX) grid of 2-D blocks (E/W ghost columns) instead of y-slabs")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=5, help="timed repetitions of --steps steps (median reported)")
+    ap.add_argument("--sustained-s", type=float, default=1.5,
+                    help="length of the extra sustained run (power-cap steady state), 0 to skip")
+    ap.add_argument("--check-steps", type=int, default=3,
+                    help="N>1: steps of the peer-path self-check against a reference path before timing")
+    ap.add_argument("--inject-peer-fault", action="store_true",
+                    help="test: rank 1 reports a self-check mismatch (exercises the fallback decision)")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 with gloo for the host-side collectives "
                          "(peer-memory path only: NCCL refuses two ranks on one GPU); not a scaling measurement")
@@ -268,6 +308,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    args.reps = max(1, args.reps)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -305,12 +346,20 @@ def main():
     # N > 1: the fused peer-memory path by default (each step ONE kernel: flux,
     # update, halo rows/columns stored into the neighbours' ghost cells over
     # NVLink, CFL max-all-reduce by system-scope atomics in its last CTA); the
-    # NCCL path is the baseline (--nccl) and the fallback if CUDA IPC between
-    # the ranks fails (decided collectively, so every rank takes the same path)
+    # NCCL path is the measured baseline (nccl_baseline in the line; --nccl to
+    # time it alone) and the fallback if CUDA IPC between the ranks fails or
+    # the peer path's self-check disagrees (decided collectively, so every rank
+    # takes the same path)
     peer = world > 1 and not args.nccl
+    have_nccl = world > 1 and not args.shared_gpu
     stream = torch.cuda.current_stream()
     spray = system == "spray"
     base_flags = (fv2d.FLAG_NAIVE if args.naive else 0) | (fv2d.FLAG_ONE_CELL if args.one_cell else 0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
 
     def make_solver(use_peer):
         nid = None
@@ -321,7 +370,10 @@ def main():
                            flags=base_flags | (fv2d.FLAG_PEER_HALO if use_peer else 0), nranks_x=px,
                            nccl_id=nid, stream=stream.cuda_stream)
 
+    clk = ClockSampler(local).__enter__()     # sampling from before the warm-up
     s = None
+    s_nccl = None
+    peer_check = None
     if peer:
         # every rank reaches every collective below whatever fails where
         h = None
@@ -339,15 +391,20 @@ def main():
             except fv2d.FV2DError as e:
                 print(f"rank {rank}: peer_connect failed ({e})", file=sys.stderr, flush=True)
                 ok = 0.0
-        (neg_ok,) = D.max_over_ranks([-ok], device="cpu" if args.shared_gpu else "cuda")
+        (neg_ok,) = D.max_over_ranks([-ok], device=red_dev)
         if -neg_ok < 1.0:  # some rank failed: all take the NCCL path
             if rank == 0:
                 print("peer-memory path unavailable on some rank: using NCCL", file=sys.stderr, flush=True)
             if s is not None:
                 s.close()
             s, peer = None, False
+            peer_check = {"ok": False, "reason": "CUDA IPC setup failed on some rank", "fallback": "nccl"}
     if s is None:
+        if args.shared_gpu and world > 1:
+            raise SystemExit("--shared-gpu: the peer-memory path is unavailable and NCCL cannot share one GPU")
         s = make_solver(False)
+    elif have_nccl:
+        s_nccl = make_solver(False)   # the baseline, the self-check reference and the fallback
     W0 = gen_ic(system, nx, ny, (j0, j1))
     if px > 1:
         W0 = np.ascontiguousarray(W0[:, i0:i1])
@@ -356,41 +413,132 @@ def main():
     if spray:
         dt = 0.5 * min(1.0 / nx, 1.0 / ny) / smax0   # R17
 
-    def steps(k):
+    def run_steps(sol, k):
         if args.adaptive:
-            s.step_adaptive(CFL, k, log=False)
+            sol.step_adaptive(CFL, k, log=False)
         else:
-            s.step(dt, k)
+            sol.step(dt, k)
 
-    steps(args.warmup)
-    s.synchronize()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    # ------------------------------------------- N > 1: peer-path self-check
+    if peer:
+        k = max(1, args.check_steps)
+        err = None
+        hp = ""
+        try:
+            s.set_state(W0)
+            run_steps(s, k)
+            hp = sha_state(s.get_state())
+        except fv2d.FV2DError as e:
+            err = str(e)
+        if s_nccl is not None:
+            ref_kind = "the NCCL path on the same ranks"
+            s_nccl.set_state(W0)
+            run_steps(s_nccl, k)
+            hr = sha_state(s_nccl.get_state())
+        else:
+            # --shared-gpu (no NCCL): rank 0 steps the whole domain as one rank
+            ref_kind = "one rank over the whole domain (rank 0)"
+            blocks = None
+            if rank == 0:
+                Wf = gen_ic(system, nx, ny, (0, ny))
+                with fv2d.Solver(nx, ny, fv2d.SPRAY if spray else fv2d.EULER,
+                                 param=(1.0, 1.0) if spray else (GAMMA,), device=local, flags=base_flags) as r1:
+                    r1.set_state(Wf)
+                    run_steps(r1, k)
+                    Wr = r1.get_state()
+                blocks = []
+                for r in range(world):
+                    b0, b1, c0, c1 = D.block_of(r, px, world // px, nx, ny)
+                    blocks.append(sha_state(Wr[b0:b1, c0:c1]))
+                del Wf, Wr
+            obj = [blocks]
+            dist.broadcast_object_list(obj, src=0)
+            hr = obj[0][rank]
+        bad = err is not None or hp != hr or (args.inject_peer_fault and rank == 1)
+        flags_bad = [0.0] * world
+        flags_bad[rank] = 1.0 if bad else 0.0
+        bad_ranks = [r for r, v in enumerate(D.max_over_ranks(flags_bad, device=red_dev)) if v > 0]
+        peer_check = {"ok": not bad_ranks, "steps": k, "reference": ref_kind, "compared": "sha256 of each rank's "
+                      "state after the steps", "mismatch_ranks": bad_ranks,
+                      **({"injected_fault": True} if args.inject_peer_fault else {})}
+        if bad_ranks:
+            if rank == 0:
+                print(f"peer-memory path self-check failed on ranks {bad_ranks}" +
+                      (" (injected)" if args.inject_peer_fault else "") + ": falling back to NCCL" +
+                      ("" if s_nccl is not None else " -- unavailable (--shared-gpu)"), file=sys.stderr, flush=True)
+            if s_nccl is None:
+                peer_check["fallback"] = "none available (--shared-gpu: no NCCL on one GPU)"
+                if rank == 0:
+                    print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                                      "error": "peer-memory self-check failed", "peer_check": peer_check}),
+                          flush=True)
+                clk.__exit__()
+                s.close()
+                dist.destroy_process_group()
+                return
+            peer_check["fallback"] = "nccl"
+            s.close()
+            s, s_nccl, peer = s_nccl, None, False
 
     # ---------------------------------------------------------------- timed
-    st0 = s.stats()
-    s.set_profiling(True)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        ev0.record(stream)
-        steps(args.steps)
-        ev1.record(stream)
-        barrier()
-    ms = ev0.elapsed_time(ev1)
-    st1 = s.stats()
-    s.set_profiling(False)
-    s.synchronize()                      # no latched CFL/non-finite error in the timed steps
-    kern_ms = st1["step_kernel_ms"] / max(1, st1["step_kernels_timed"])
-    src_ms = st1["source_kernel_ms"] / max(1, st1["source_kernels_timed"])
-    launches = st1["kernel_launches"] - st0["kernel_launches"]
-    ms_max, kern_max, src_max = D.max_over_ranks([ms, kern_ms, src_ms], device=red_dev)
+    def timed(sol, phase, k, reps):
+        """reps repetitions of exactly k steps, each bracketed by a barrier and a
+        device synchronize; CUDA events on the library's stream; per repetition
+        the max over ranks.  Returns (per-rep ms list, kernel ms, source ms, launches)."""
+        st0 = sol.stats()
+        sol.set_profiling(True)
+        per_rep = []
+        for _ in range(reps):
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            barrier()
+            clk.phase = phase
+            ev0.record(stream)
+            run_steps(sol, k)
+            ev1.record(stream)
+            barrier()
+            clk.phase = "between"
+            per_rep.append(ev0.elapsed_time(ev1))
+        st1 = sol.stats()
+        sol.set_profiling(False)
+        sol.synchronize()                      # no latched CFL/non-finite error in the timed steps
+        kern = st1["step_kernel_ms"] / max(1, st1["step_kernels_timed"])
+        src = st1["source_kernel_ms"] / max(1, st1["source_kernels_timed"])
+        red = D.max_over_ranks(per_rep + [kern, src], device=red_dev)
+        return red[:reps], red[reps], red[reps + 1], (st1["kernel_launches"] - st0["kernel_launches"]) / reps, st0, st1
+
+    s.set_state(W0)
+    run_steps(s, args.warmup)
+    s.synchronize()
+    reps_ms, kern_max, src_max, launches, st0, st1 = timed(s, "timed", args.steps, args.reps)
+    ms_max = float(np.median(reps_ms))
     cells_total = nx * ny
     value = cells_total * args.steps / (ms_max * 1e-3)
+    newton = (st1["newton_iters"] - st0["newton_iters"]) / ((i1 - i0) * H * args.steps * args.reps)
+
+    sustained = None
+    if args.sustained_s > 0:
+        nsus = max(args.steps, int(np.ceil(args.sustained_s * 1e3 / (ms_max / args.steps))))
+        sus_ms, sus_kern, sus_src, _, _, _ = timed(s, "sustained", nsus, 1)
+        sustained = {"steps": nsus, "seconds": sus_ms[0] / 1e3, "ms_per_step": sus_ms[0] / nsus,
+                     "value": cells_total * nsus / (sus_ms[0] * 1e-3), "kernel_ms": sus_kern,
+                     "source_kernel_ms": sus_src if spray else None, "clocks": clk.summary("sustained")}
+
+    nccl_baseline = None
+    if s_nccl is not None:
+        # the north_star's mechanism, timed on the same ranks and workload
+        s_nccl.set_state(W0)
+        run_steps(s_nccl, args.warmup)
+        s_nccl.synchronize()
+        n_ms, n_kern, _, n_launch, _, _ = timed(s_nccl, "nccl", args.steps, args.reps)
+        nm = float(np.median(n_ms))
+        nccl_baseline = {"ms_per_step": nm / args.steps, "value": cells_total * args.steps / (nm * 1e-3),
+                         "ms_per_step_min": min(n_ms) / args.steps, "ms_per_step_max": max(n_ms) / args.steps,
+                         "interior_kernel_ms": n_kern, "gpu_launches": n_launch,
+                         "path": "boundary rows + NCCL send/recv on a comm stream overlapped with the interior "
+                                 "launch, ncclAllReduce(max) of [smax, status], finalize kernel"}
+        s_nccl.close()
+        s_nccl = None
 
     # ---------------------------------------------------------------- e2e
     e2e = None
@@ -400,6 +548,7 @@ def main():
         ptr = hostbuf.data_ptr()
         s.set_state_ptr(ptr)
         barrier()
+        clk.phase = "e2e"
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -409,13 +558,17 @@ def main():
             s.step_host(ptr, ptr, dt, 1)
         e1.record(stream)
         barrier()
+        clk.phase = "between"
         (et,) = D.max_over_ranks([e0.elapsed_time(e1)], device=red_dev)
         nbytes = W0.size * 8
         e2e = {"value": cells_total * args.e2e_steps / (et * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
-               "api": "fv2d_step_host(host AoS in -> host AoS out, pinned, in place; banded copy/compute overlap" +
-                      ("; a new W^0 each step, so the source's Newton starts cold)" if spray else ")")}
+               "api": "fv2d_step_host(host AoS in -> host AoS out, pinned, in place" +
+                      ("; the spray's first step needs all of W^0 on the device for the S:440 guard, so its "
+                       "copies are not overlapped; a new W^0 each step, so the source's Newton starts cold)"
+                       if spray else "; banded copy/compute overlap)")}
         del hostbuf
+    clk.__exit__()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -431,7 +584,9 @@ def main():
         traffic = ncu_traffic(kernel)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                    "bytes_per_cell": bpc, "kernel_ms": kern_max, "cells_per_launch": cells_per_launch}
+                    "bytes_per_cell": bpc, "kernel_ms": kern_max, "cells_per_launch": cells_per_launch,
+                    **({"sustained_frac": bpc * cells_per_launch / (sustained["kernel_ms"] * 1e-3) / 1e9 / peak}
+                       if sustained else {})}
         if spray:
             # the dominant kernel is the source pass: FP64-bound (arithmetic intensity
             # ~14 flop/B, far above the FP64 ridge of ~5.7 flop/B)
@@ -446,6 +601,8 @@ def main():
                         "(profiles/ncu_summary.json), steady state", "kernel_ms": src_max,
                         "cells_per_launch": cells_per_launch,
                         "arithmetic_intensity_flop_per_byte": prof["arithmetic_intensity_flop_per_byte"],
+                        **({"sustained_frac": fpc * cells_per_launch / (sustained["source_kernel_ms"] * 1e-3)
+                            / 1e12 / FP64_PEAK_TFLOPS} if sustained else {}),
                         "transport_kernel": {"bound": "hbm", "achieved_gbs": achieved, "peak_gbs": peak,
                                              "frac": achieved / peak, "bytes_per_cell": bpc,
                                              "kernel_ms": kern_max}}
@@ -454,12 +611,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
+            "repetitions": args.reps, "ms_per_step_min": min(reps_ms) / args.steps,
+            "ms_per_step_max": max(reps_ms) / args.steps,
+            "timing": f"median of {args.reps} repetitions of exactly {args.steps} steps, each bracketed by a "
+                      "barrier + cudaDeviceSynchronize, CUDA events on the library's stream, max over ranks",
             "config": {"workload": args.workload, "description": desc, "nx": nx, "ny": ny,
                        "rows_per_gpu": H, "cols_per_gpu": i1 - i0,
                        "mode": "adaptive dt" if args.adaptive else "fixed dt (checked)",
                        "dt": dt, "kernel": kernel,
-                       **({"newton_iters_per_cell_step": (st1["newton_iters"] - st0["newton_iters"]) /
-                           (cells_per_launch * args.steps)} if spray else {}),
+                       **({"newton_iters_per_cell_step": newton} if spray else {}),
                        "parallelism": (f"y-slabs x{world}" if px == 1 else f"2-D blocks {px}x{world // px}") + (
                            (" (peer memory: halo stores + all-reduce fused in the step kernel)" if peer else
                             " (NCCL halo overlapped + all-reduce)")
@@ -471,7 +631,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clk.summary("timed"),
+            "sustained": sustained,
+            **({"peer_check": peer_check, "nccl_baseline": nccl_baseline} if world > 1 else {}),
         }
         print(json.dumps(out), flush=True)
     s.close()

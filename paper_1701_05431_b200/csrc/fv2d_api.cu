@@ -67,7 +67,7 @@ bool load_nccl() {
 // ------------------------------------------------------------------ GL-24 table
 // Gauss-Legendre nodes/weights on [0,1] by Newton's method on P_24 in long
 // double; uploaded once to constant memory.
-void gl24_table(double t[24], double wt[24][8]) {
+void gl24_table(double t[24], double wt[24][kGLW]) {
   const int n = 24;
   for (int k = 0; k < n; ++k) {
     long double x = cosl(3.14159265358979323846264338327950288L * (k + 0.75L) / (n + 0.5L));
@@ -96,7 +96,7 @@ void gl24_table(double t[24], double wt[24][8]) {
     t[q] = (double)((x + 1) / 2);
     const double wq = (double)(w / 2);
     double tp = 1.0;
-    for (int m = 0; m < 8; ++m) {
+    for (int m = 0; m < kGLW; ++m) {
       wt[q][m] = wq * tp;
       tp = tp * t[q];
     }
@@ -193,8 +193,14 @@ struct fv2d_ctx {
   bool has_state = false;
   bool dt_valid = false;
   double dt_cfl = 0.0;       // the C that dt_dev was computed with (adaptive mode)
+  // pinned scratch for the small host<->device scalars (status, smax, dt): a
+  // copy to/from pageable memory is staged by the driver and can wait behind
+  // another rank's spinning collective in the same process (peer path, ranks
+  // as threads), which then never sees this rank arrive
+  unsigned long long* hpin = nullptr;
   int sms = 0;               // multiprocessors of cfg.device
   int slots = 0;             // resident CTAs of the marching step kernel (sms x occupancy)
+  int src_slots = 0;         // resident CTAs of the spray source pass (its persistent grid)
   bool guard_done = false;   // S:440 guard passed since the last set_state
   long long steps = 0;
   long long launches = 0;
@@ -583,7 +589,19 @@ cudaError_t query_geometry(fv2d_ctx* ctx) {
   }
   if (e != cudaSuccess) return e;
   ctx->slots = ctx->sms * std::max(1, per_sm);
+  if (ctx->cfg.system == FV2D_SPRAY) {
+    int src = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&src, spray_source_step_kernel, kSrcThreads, 0);
+    if (e != cudaSuccess) return e;
+    ctx->src_slots = ctx->sms * std::max(1, src);
+  }
   return cudaSuccess;
+}
+
+// Persistent grid of the spray source pass over `rows` rows of `nslabs` slabs.
+dim3 src_grid(const fv2d_ctx* ctx, int rows, int nslabs) {
+  const long long tiles = (long long)rows * ((ctx->nx + kSrcThreads - 1) / kSrcThreads) * nslabs;
+  return dim3((unsigned)std::max<long long>(1, std::min<long long>(tiles, std::max(1, ctx->src_slots))));
 }
 
 // Load every kernel a context can launch, and set the pair kernels' dynamic
@@ -642,6 +660,7 @@ struct Preload {
     t(touch(promote_pending_kernel));
     t(touch(spray_source_kernel));
     t(touch(spray_source_step_kernel));
+    t(touch(spray_guard_kernel));
     t(touch(fill_halo_kernel));
     t(touch(fill_halo_cols_kernel));
     t(touch(unpack_col_kernel));
@@ -717,6 +736,8 @@ fv2d_status allreduce_scalars(fv2d_ctx* ctx, cudaStream_t stream = nullptr) {
 
 // One collective point of the peer path: max-all-reduce dscal[0..1] -> dscal[4..5].
 fv2d_status peer_collective(fv2d_ctx* ctx, cudaStream_t stream) {
+  static const bool dbg = getenv("FV2D_DEBUG_PEER") != nullptr;
+  if (dbg) fprintf(stderr, "[fv2d] rank %d collective epoch %llu steps %lld\n", ctx->cfg.rank, ctx->epoch, ctx->steps);
   peer_collective_kernel<<<1, 32, 0, stream>>>(ctx->pa, ctx->dscal + 0, ctx->dscal + 4, ctx->epoch, ctx->dscal + 2);
   ++ctx->epoch;
   ++ctx->launches;
@@ -748,12 +769,16 @@ fv2d_status ensure_dt_log(fv2d_ctx* ctx, long long need) {
   return FV2D_OK;
 }
 
-fv2d_status read_status(fv2d_ctx* ctx, unsigned long long* st_out) {
-  unsigned long long st = 0;
-  CK(cudaMemcpyAsync(&st, ctx->dscal + 2, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+// Device -> host copy of n (<= 8) words through the pinned scratch, synchronous.
+fv2d_status d2h_words(fv2d_ctx* ctx, unsigned long long* dst, const unsigned long long* src, int n) {
+  CK(cudaMemcpyAsync(ctx->hpin, src, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  *st_out = st;
+  memcpy(dst, ctx->hpin, n * sizeof(unsigned long long));
   return FV2D_OK;
+}
+
+fv2d_status read_status(fv2d_ctx* ctx, unsigned long long* st_out) {
+  return d2h_words(ctx, st_out, ctx->dscal + 2, 1);
 }
 
 // Translate a latched status word into an error code + description.
@@ -769,12 +794,13 @@ fv2d_status reduce_current(fv2d_ctx* ctx, double* smax_out, unsigned long long* 
   if (ctx->use_nccl || ctx->peer) {
     fv2d_status s = reduce_ranks(ctx, ctx->stream);
     if (s) return s;
-    CK(cudaMemcpyAsync(h, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->hpin, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   } else {
-    CK(cudaMemcpyAsync(h, ctx->dscal + 0, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->hpin, ctx->dscal + 0, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  memcpy(h, ctx->hpin, sizeof h);
   double s;
   memcpy(&s, &h[0], sizeof s);
   *smax_out = s;
@@ -788,8 +814,7 @@ fv2d_status report(fv2d_ctx* ctx, unsigned long long st) {
   const long long step = (long long)(st & 0x00FFFFFFFFFFFFFFull);
   ctx->err_step = step;
   unsigned long long bc = ~0ull;
-  if (cudaMemcpyAsync(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess)
-    cudaStreamSynchronize(ctx->stream);
+  if (d2h_words(ctx, &bc, ctx->dscal + 3, 1) != FV2D_OK) bc = ~0ull;
   ctx->err_cell = bc == ~0ull ? -1 : (long long)bc;
   switch (code) {
     case ST_CFL:
@@ -818,8 +843,8 @@ fv2d_status diagnose(fv2d_ctx* ctx, unsigned long long st) {
     dispatch<LaunchReduce>(ctx->cfg.system, ctx, a);
     CKL();
     unsigned long long h[2];
-    CK(cudaMemcpyAsync(h, ctx->dscal, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    fv2d_status s2 = d2h_words(ctx, h, ctx->dscal, 2);
+    if (s2) return s2;
     double smax;
     memcpy(&smax, &h[0], sizeof smax);
     if (code == ST_CFL) {
@@ -889,6 +914,7 @@ fv2d_status fv2d_destroy(fv2d_ctx* ctx) {
   if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
   if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   if (ctx->dscal) cudaFree(ctx->dscal);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
   if (ctx->done) cudaFree(ctx->done);
   if (ctx->dt_dev) cudaFree(ctx->dt_dev);
   if (ctx->dt_log) cudaFree(ctx->dt_log);
@@ -1031,6 +1057,7 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
     CKC(cudaMemset(ctx->sync, 0, sizeof(PeerSync)));
   }
   CKC(cudaMalloc(&ctx->dscal, 8 * sizeof(unsigned long long)));
+  CKC(cudaHostAlloc(&ctx->hpin, 16 * sizeof(unsigned long long), cudaHostAllocPortable));
   CKC(cudaMemset(ctx->dscal, 0, 8 * sizeof(unsigned long long)));
   CKC(cudaMemset(ctx->dscal + 3, 0xff, sizeof(unsigned long long)));
   CKC(cudaMalloc(&ctx->done, sizeof(unsigned int)));
@@ -1057,10 +1084,13 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
       static std::set<int> gl_devices;
       std::lock_guard<std::mutex> lk(gl_mu);
       if (!gl_devices.count(c.device)) {
-        double t[24], wt[24][8];
+        double t[24], wt[24][kGLW];
         gl24_table(t, wt);
         CKC(cudaMemcpyToSymbol(c_gl_t, t, sizeof t));
         CKC(cudaMemcpyToSymbol(c_gl_wt, wt, sizeof wt));
+        double e2[64];  // 2^(j/64), correctly rounded from long double (exp_tab)
+        for (int jj = 0; jj < 64; ++jj) e2[jj] = (double)exp2l((long double)jj / 64.0L);
+        CKC(cudaMemcpyToSymbol(c_exp2_64, e2, sizeof e2));
         gl_devices.insert(c.device);
       }
     }
@@ -1120,14 +1150,15 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   }
   fv2d_status st = exchange(ctx, 0);
   if (st) return st;
-  unsigned long long init[8] = {0, 0, 0, ~0ull, 0, 0, 0, 0};
   if (ctx->peer) {
     // barrier: every rank has written its halo rows into its neighbours' ghost rows
     CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
     st = peer_collective(ctx, ctx->stream);
     if (st) return st;
   }
-  CK(cudaMemcpyAsync(ctx->dscal, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  // dscal = {0, 0, 0, ~0, 0, 0, 0, 0} (no pageable host source, see hpin)
+  CK(cudaMemsetAsync(ctx->dscal, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->done, 0, sizeof(unsigned int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dt_dev, 0, sizeof(double), ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1242,7 +1273,8 @@ fv2d_status fv2d_compute_dt(fv2d_ctx* ctx, double cfl, double* dt, double* smax)
   }
   const double d = (cfl * ctx->hmin) / s;
   if (dt) *dt = d;
-  CK(cudaMemcpyAsync(ctx->dt_dev, &d, sizeof d, cudaMemcpyHostToDevice, ctx->stream));
+  memcpy(ctx->hpin + 8, &d, sizeof d);
+  CK(cudaMemcpyAsync(ctx->dt_dev, ctx->hpin + 8, sizeof d, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->dt_valid = true;
   ctx->dt_cfl = cfl;
@@ -1331,6 +1363,8 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
     a.fused_finalize = 1;
     a.peer_fused = 1;
     a.peer = ctx->pa;
+    static const bool dbg = getenv("FV2D_DEBUG_PEER") != nullptr;
+    if (dbg) fprintf(stderr, "[fv2d] rank %d step collective epoch %llu steps %lld\n", ctx->cfg.rank, ctx->epoch, ctx->steps);
     a.peer_epoch = ctx->epoch++;
   }
   StepArgs at = a;  // transport pass
@@ -1407,7 +1441,7 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
   if (split) {
     // in place on the transport output; dt: the fixed dt, or read from the
     // device in adaptive mode (the finalize writes dt_{n+1} only after this pass)
-    dim3 grid((ctx->nx + kSrcThreads - 1) / kSrcThreads, std::min(ctx->H, 65535), ctx->nslabs);
+    const dim3 grid = src_grid(ctx, ctx->H, ctx->nslabs);
     StepArgs b = a;
     if (tiled) b.fused_finalize = 0;
     cudaEvent_t s0 = nullptr, s1 = nullptr;
@@ -1542,12 +1576,13 @@ static fv2d_status spray_guard(fv2d_ctx* ctx, double dt, bool fixed) {
   if (ctx->use_nccl || ctx->peer) {
     s0 = reduce_ranks(ctx, ctx->stream);
     if (s0) return s0;
-    CK(cudaMemcpyAsync(&h, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->hpin, ctx->dscal + 4, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   } else {
-    CK(cudaMemcpyAsync(&h, ctx->dscal + 0, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->hpin, ctx->dscal + 0, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaMemsetAsync(ctx->dscal, 0, 2 * sizeof(unsigned long long), ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  h = ctx->hpin[0];
   const double rmin = h ? min_key_decode(h) : INFINITY;
   const double K = ctx->cfg.param[0];
   if ((dt * K) > (0.1 * rmin)) {
@@ -1555,7 +1590,8 @@ static fv2d_status spray_guard(fv2d_ctx* ctx, double dt, bool fixed) {
     spray_guard_kernel<<<grid, 256, 0, ctx->stream>>>(a, nullptr, rmin, ctx->dscal + 3);
     CKL();
     unsigned long long cell = ~0ull;
-    CK(cudaMemcpyAsync(&cell, ctx->dscal + 3, sizeof cell, cudaMemcpyDeviceToHost, ctx->stream));
+    s0 = d2h_words(ctx, &cell, ctx->dscal + 3, 1);
+    if (s0) return s0;
     CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->err_step = 0;
@@ -1646,8 +1682,8 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
     CK(cudaEventRecord(ev_in[b], ctx->h2d_stream));
   }
   // reset the step's device scalars as after_set_state does
-  unsigned long long init[8] = {0, 0, 0, ~0ull, 0, 0, 0, 0};
-  CK(cudaMemcpyAsync(ctx->dscal, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->dscal, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->done, 0, sizeof(unsigned int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dt_dev, 0, sizeof(double), ctx->stream));
   ctx->lam_hist = 0;  // a new W^0: the spray source starts Newton cold (R19)
@@ -1686,8 +1722,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
       StepArgs sb = a;
       sb.src_row_lo = lo(b);
       sb.src_row_hi = hi(b);
-      dim3 grid((nx + kSrcThreads - 1) / kSrcThreads, std::min(hi(b) - lo(b), 65535), 1);
-      spray_source_dt_kernel_launch(ctx, sb, grid, 0);
+      spray_source_dt_kernel_launch(ctx, sb, src_grid(ctx, hi(b) - lo(b), 1), 0);
       CKL();
     }
     dev_to_aos_kernel<<<num_sms(ctx) * 2, 256, 0, ctx->stream>>>(row_ptr(ctx, 0, 1, lo(b)), ctx->staging_out + row_doubles * lo(b),
@@ -1763,6 +1798,18 @@ fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_ou
     st = fv2d_set_state(ctx, host_in, layout);
     if (st) return st;
     st = fv2d_step(ctx, dt, nsteps);
+    if (st == FV2D_E_ARG) {  // the S:440 guard: no step taken, host_out receives W^0
+      const std::string msg = ctx->err;
+      const long long cell = ctx->err_cell;
+      const double val = ctx->err_value;
+      fv2d_status g = fv2d_get_state(ctx, host_out, layout);
+      if (g) return g;
+      ctx->err = msg;
+      ctx->err_step = 0;
+      ctx->err_cell = cell;
+      ctx->err_value = val;
+      return FV2D_E_ARG;
+    }
     if (st) return st;
   }
   return fv2d_get_state(ctx, host_out, layout);
@@ -1787,8 +1834,7 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   b.lam_in = ctx->lam_buf[p];
   b.lam_out = ctx->lam_buf[p];
   b.lam_old = nullptr;
-  dim3 grid((ctx->nx + kSrcThreads - 1) / kSrcThreads, std::min(ctx->H, 65535), ctx->nslabs);
-  spray_source_kernel<<<grid, kSrcThreads, 0, ctx->stream>>>(b, dt, 0);
+  spray_source_kernel<<<src_grid(ctx, ctx->H, ctx->nslabs), kSrcThreads, 0, ctx->stream>>>(b, dt, 0);
   CKL();
   ctx->lam_hist = 1;
   fv2d_status st = exchange(ctx, p);
@@ -1832,8 +1878,7 @@ fv2d_status fv2d_last_error(fv2d_ctx* ctx, char* buf, size_t n, int64_t* step, i
     report(ctx, st);
     diagnose(ctx, st);
     unsigned long long bc = ~0ull;
-    if (cudaMemcpyAsync(&bc, ctx->dscal + 3, sizeof bc, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess)
-      cudaStreamSynchronize(ctx->stream);
+    if (d2h_words(ctx, &bc, ctx->dscal + 3, 1) != FV2D_OK) bc = ~0ull;
     ctx->err_cell = bc == ~0ull ? -1 : (long long)bc;
   }
   if (buf && n) {
@@ -2030,12 +2075,12 @@ fv2d_status fv2d_get_stats(fv2d_ctx* ctx, fv2d_stats* out) {
   out->resident_ctas = ctx->slots;
   out->strip_rows = ctx->rps;
   out->reserved0 = 0;
-  unsigned long long ni = 0;
-  if (ctx->newton) cudaMemcpyAsync(&ni, ctx->newton, sizeof ni, cudaMemcpyDeviceToHost, ctx->stream);
+  unsigned long long ni = 0, dbits = 0;
+  if (ctx->newton) d2h_words(ctx, &ni, ctx->newton, 1);
   out->newton_iters = (int64_t)ni;
-  double d = 0;
-  if (ctx->dt_dev) cudaMemcpyAsync(&d, ctx->dt_dev, sizeof d, cudaMemcpyDeviceToHost, ctx->stream);
-  cudaStreamSynchronize(ctx->stream);
+  if (ctx->dt_dev) d2h_words(ctx, &dbits, reinterpret_cast<const unsigned long long*>(ctx->dt_dev), 1);
+  double d;
+  memcpy(&d, &dbits, sizeof d);
   out->dt = d;
   return FV2D_OK;
 }

@@ -335,4 +335,5 @@ class Solver:
         self._check(lib().fv2d_get_stats(self._h, C.byref(s)), "get_stats")
         return {"steps": s.steps, "kernel_launches": s.kernel_launches, "newton_iters": s.newton_iters,
                 "dt": s.dt, "step_kernel_ms": s.step_kernel_ms, "step_kernels_timed": s.step_kernels_timed,
-                "source_kernel_ms": s.source_kernel_ms, "source_kernels_timed": s.source_kernels_timed}
+                "source_kernel_ms": s.source_kernel_ms, "source_kernels_timed": s.source_kernels_timed,
+                "sms": s.sms, "resident_ctas": s.resident_ctas, "strip_rows": s.strip_rows}

@@ -42,8 +42,14 @@ def test_bench_json_contract_on_gpu():
     rf = d["roofline"]
     assert rf["bound"] == "hbm" and 0 < rf["frac"] < 1.5 and rf["unit"] == "GB/s"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+    assert d["cpu_baseline"]["host_cores"] >= 1 and "cpu_model" in d["cpu_baseline"]
     assert d["e2e"]["h2d_bytes_per_step"] == 1024 * 1024 * 32 and d["e2e"]["value"] > 0
     assert d["config"]["workload"] == "c2_euler_1024"
+    # protocol: median of repetitions, in-process clock samples inside the timed region, sustained run
+    assert d["repetitions"] == 5 and d["ms_per_step_min"] <= d["ms_per_step"] <= d["ms_per_step_max"]
+    assert d["clocks"]["samples"] > 0 and d["clocks"]["sm_mhz"] > 0
+    assert d["sustained"]["seconds"] >= 1.0 and d["sustained"]["clocks"]["samples"] > 50
+    assert 0 < d["roofline"]["sustained_frac"] < 1.5
 
 
 @pytest.mark.gpu
@@ -71,6 +77,33 @@ def test_bench_multi_rank_launch_on_one_gpu(px):
     assert d["config"]["test_mode"].startswith("all ranks share cuda:0")
     assert ("2-D blocks 2x1" if px == 2 else "y-slabs x2") in d["config"]["parallelism"]
     assert d["cpu_baseline"] is None and d["e2e"]["value"] > 0
+    pc = d["peer_check"]
+    assert pc["ok"] is True and pc["steps"] == 3 and pc["reference"].startswith("one rank over the whole domain")
+    assert d["nccl_baseline"] is None        # NCCL cannot put two ranks on one GPU
+
+
+@pytest.mark.gpu
+def test_bench_peer_self_check_forced_failure():
+    """--inject-peer-fault: rank 1 reports a self-check mismatch; every rank
+    takes the same decision (fall back to NCCL -- which --shared-gpu cannot
+    provide, so the line reports the failed check instead of a number) and the
+    run exits cleanly instead of timing a path it cannot trust."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--shared-gpu", "--workload", "c2_euler_1024", "--steps", "5", "--warmup", "3", "--inject-peer-fault"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["value"] is None and d["peer_check"]["ok"] is False and d["peer_check"]["mismatch_ranks"] == [1]
+    assert d["peer_check"]["fallback"].startswith("none available")
+    assert "falling back to NCCL" in r.stderr
 
 
 def test_reference_arm_spray_workload():

@@ -34,3 +34,31 @@ for i in range(20000):
     ulp=float(err)/2.220446049250313e-16
     worst=max(worst,ulp)
 print("LN2_LO",repr(LN2_LO),"worst ulp (rel err / eps):",worst)
+
+# exp_tab (FV2D_EXP_TAB): 2^k * 2^(j/64) * e^r, |r| <= ln2/128, degree-5 Estrin
+x64 = decimal.Decimal(64) / ln2
+C64 = float(x64)
+L1 = float(ln2 / 64)
+L2 = float(ln2 / 64 - decimal.Decimal(L1))
+TAB = [float(decimal.Decimal(2) ** (decimal.Decimal(j) / 64)) for j in range(64)]
+def exptab(x):
+    if x > 709.0: return float('inf')
+    tm = fma(x, C64, 6755399441055744.0)
+    nd = tm - 6755399441055744.0
+    n = int(nd)
+    r = fma(nd, -L1, x); r = fma(nd, -L2, r)
+    r2 = r * r
+    a0 = r + 1.0
+    a1 = fma(r, 1.0 / 6.0, 0.5)
+    a2 = fma(r, 1.0 / 120.0, 1.0 / 24.0)
+    b0 = fma(a1, r2, a0)
+    r4 = r2 * r2
+    p = fma(a2, r4, b0)
+    k = max(min(n >> 6, 1023), -1022)
+    return p * math.ldexp(TAB[n & 63], k)
+random.seed(2); worst = 0
+for i in range(20000):
+    x = random.uniform(-40, 40) if i % 2 else random.uniform(-700, 700)
+    y = exptab(x); ex = decimal.Decimal(x).exp()
+    worst = max(worst, float(abs((decimal.Decimal(y) - ex) / ex)) / 2.220446049250313e-16)
+print("exp_tab: C64", repr(C64), "L1", repr(L1), "L2", repr(L2), "worst ulp (rel err / eps):", worst)
