@@ -111,16 +111,24 @@ class ClockSampler:
             self._err = repr(e)
         return self
 
-    def _run(self):
+    def sample_now(self):
+        """One sample from the calling thread (the timed loop calls this right
+        after issuing a repetition's steps, while the GPU runs them, so even a
+        repetition shorter than the 10 ms period has a sample)."""
+        if self._nvml is None:
+            return
         N, h = self._nvml, self._h
+        try:
+            sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+            rs = int(N.nvmlDeviceGetCurrentClocksEventReasons(h))
+            pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+            self.samples.append((self.phase, sm, rs, pw))
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-                rs = int(N.nvmlDeviceGetCurrentClocksEventReasons(h))
-                pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
-                self.samples.append((self.phase, sm, rs, pw))
-            except Exception:
-                pass
+            self.sample_now()
             self._stop.wait(0.01)
 
     def __exit__(self, *a):
@@ -495,6 +503,7 @@ def main():
             clk.phase = phase
             ev0.record(stream)
             run_steps(sol, k)
+            clk.sample_now()
             ev1.record(stream)
             barrier()
             clk.phase = "between"

@@ -201,6 +201,7 @@ struct fv2d_ctx {
   int sms = 0;               // multiprocessors of cfg.device
   int slots = 0;             // resident CTAs of the marching step kernel (sms x occupancy)
   int src_slots = 0;         // resident CTAs of the spray source pass (its persistent grid)
+  int fused_slots = 0;       // resident CTAs of the fused spray step (its persistent grid)
   bool guard_done = false;   // S:440 guard passed since the last set_state
   long long steps = 0;
   long long launches = 0;
@@ -476,6 +477,43 @@ void launch_pair(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
   else launch_pair_x<Sys, D, XM_CLAMP>(ctx, a, grid);
 }
 
+// The fused spray step (spray_fused_step_kernel): persistent grid of
+// fused_slots 64-thread CTAs, i.e. 2 x fused_slots independent warps, each
+// marching items of 32 columns x one strip of rows.  Strip height per row
+// range: minimise waves x (rows + halo/8) over 2..64 rows -- a halo row costs a
+// load and a derive, an owned row also the Newton reconstruction (~30x more).
+int pick_rps_fused(const fv2d_ctx* ctx, int ncols, int nrows) {
+  const long long C = (ncols + 31) / 32;
+  const long long warps = 2LL * std::max(1, ctx->fused_slots);
+  long long best = -1;
+  int best_rps = std::min(nrows, 64);
+  for (int rps = 2; rps <= 64; ++rps) {
+    const long long S = (nrows + rps - 1) / rps;
+    const long long cost = ((C * S + warps - 1) / warps) * (8LL * rps + 2);
+    if (best < 0 || cost < best) {
+      best = cost;
+      best_rps = rps;
+    }
+    if (rps >= nrows) break;
+  }
+  return std::max(1, std::min(best_rps, nrows));
+}
+
+void launch_fused(const fv2d_ctx* ctx, const StepArgs& a0) {
+  StepArgs a = a0;
+  const int ncols = a.col_hi - a.col_lo;
+  set_ranges(a, a.row_lo[0], a.row_hi[0], pick_rps_fused(ctx, ncols, a.row_hi[0] - a.row_lo[0]), a.row_lo[1],
+             a.nranges > 1 ? a.row_hi[1] : a.row_lo[1],
+             a.nranges > 1 ? pick_rps_fused(ctx, ncols, a.row_hi[1] - a.row_lo[1]) : 1);
+  const long long items = (long long)total_strips(a) * ((ncols + 31) / 32) * ctx->nslabs;
+  const long long ctas = std::max<long long>(1, std::min<long long>((items + 1) / 2, std::max(1, ctx->fused_slots)));
+  const dim3 grid((unsigned)ctas);
+  cudaStream_t ls = ctx->launch_stream;
+  if (ctx->xg) spray_fused_step_kernel<XM_GHOST><<<grid, kSrcThreads, 0, ls>>>(a);
+  else if (ctx->cfg.bc_x == FV2D_BC_PERIODIC) spray_fused_step_kernel<XM_PERIODIC><<<grid, kSrcThreads, 0, ls>>>(a);
+  else spray_fused_step_kernel<XM_CLAMP><<<grid, kSrcThreads, 0, ls>>>(a);
+}
+
 template <class Sys>
 struct LaunchStep {
   static void run(const fv2d_ctx* ctx, const StepArgs& a) {
@@ -487,20 +525,17 @@ struct LaunchStep {
       const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC && !ctx->xg;
       // spray (nVar 6) uses the one-cell kernel: its fused source needs the registers
       if constexpr (Sys::NV == 6) {
+        if (a.fuse_source) {  // transport + source in one pass
+          launch_fused(ctx, a);
+          return;
+        }
         const int cols = 30 * kWarps;
         dim3 grid((a.col_hi - a.col_lo + cols - 1) / cols, total_strips(a), ctx->nslabs);
         cudaStream_t ls = ctx->launch_stream;
-        if (a.fuse_source) {
-          if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
-          if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
-          if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
-          if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
-        } else {  // split source: the transport pass without the fused-source code
-          if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
-          if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
-          if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
-          if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D, false><<<grid, kWarps * 32, 0, ls>>>(a);
-        }
+        if (xper && !a.adaptive) fv_step_kernel<Sys, true, false, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
+        if (xper && a.adaptive) fv_step_kernel<Sys, true, true, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
+        if (!xper && !a.adaptive) fv_step_kernel<Sys, false, false, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
+        if (!xper && a.adaptive) fv_step_kernel<Sys, false, true, kWarps, D><<<grid, kWarps * 32, 0, ls>>>(a);
       } else if (ctx->cfg.flags & FV2D_FLAG_ONE_CELL) {
         const int cols = 30 * kWarps;
         dim3 grid((a.col_hi - a.col_lo + cols - 1) / cols, total_strips(a), ctx->nslabs);
@@ -549,9 +584,6 @@ struct Occupancy {
     constexpr int D = 4;
     const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC && !ctx->xg;
     if constexpr (Sys::NV == 6) {  // the one-cell kernel (LaunchStep)
-      if (!(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE))
-        return xper ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, true, false, kWarps, D, false>, kWarps * 32, 0)
-                    : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, false, false, kWarps, D, false>, kWarps * 32, 0);
       return xper ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, true, false, kWarps, D>, kWarps * 32, 0)
                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fv_step_kernel<Sys, false, false, kWarps, D>, kWarps * 32, 0);
     } else {
@@ -594,6 +626,10 @@ cudaError_t query_geometry(fv2d_ctx* ctx) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&src, spray_source_step_kernel, kSrcThreads, 0);
     if (e != cudaSuccess) return e;
     ctx->src_slots = ctx->sms * std::max(1, src);
+    int fu = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fu, spray_fused_step_kernel<XM_PERIODIC>, kSrcThreads, 0);
+    if (e != cudaSuccess) return e;
+    ctx->fused_slots = ctx->sms * std::max(1, fu);
   }
   return cudaSuccess;
 }
@@ -650,10 +686,9 @@ struct Preload {
     t(touch(fv_step_kernel<Sys, false, false, kWarps, 4>));
     t(touch(fv_step_kernel<Sys, false, true, kWarps, 4>));
     if constexpr (Sys::NV == 6) {
-      t(touch(fv_step_kernel<Sys, true, false, kWarps, 4, false>));
-      t(touch(fv_step_kernel<Sys, true, true, kWarps, 4, false>));
-      t(touch(fv_step_kernel<Sys, false, false, kWarps, 4, false>));
-      t(touch(fv_step_kernel<Sys, false, true, kWarps, 4, false>));
+      t(touch(spray_fused_step_kernel<XM_CLAMP>));
+      t(touch(spray_fused_step_kernel<XM_PERIODIC>));
+      t(touch(spray_fused_step_kernel<XM_GHOST>));
     }
     t(touch(finalize_kernel));
     t(touch(peer_collective_kernel));
@@ -1542,7 +1577,10 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
       st = issue_step(ctx, p, adaptive, dt, cfl, e1);
       if (st) return st;
     }
-    if (split) ctx->lam_hist = std::min(2, ctx->lam_hist + 1);
+    // the source pass, or the fused spray step, wrote this step's multipliers
+    // (the paper-style kernel's fused source starts every Newton cold)
+    if (split || (ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_NAIVE)))
+      ctx->lam_hist = std::min(2, ctx->lam_hist + 1);
     ctx->steps += 1;
   }
   return FV2D_OK;
