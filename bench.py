@@ -610,6 +610,12 @@ def main():
                         "(profiles/ncu_summary.json), steady state", "kernel_ms": src_max,
                         "cells_per_launch": cells_per_launch,
                         "arithmetic_intensity_flop_per_byte": prof["arithmetic_intensity_flop_per_byte"],
+                        # the same kernel against the FP64 pipe's INSTRUCTION rate (a DADD or DMUL
+                        # occupies the pipe like a DFMA but counts 1 flop, so a mixed kernel cannot
+                        # reach the DFMA flop peak): 148 SMs x 64 lanes x 1.965 GHz
+                        "fp64_instr_per_cell": prof["fp64_instr_per_cell"],
+                        "fp64_instr_frac": prof["fp64_instr_per_cell"] * cells_per_launch / (src_max * 1e-3)
+                        / (FP64_PEAK_TFLOPS * 1e12 / 2),
                         **({"sustained_frac": fpc * cells_per_launch / (sustained["source_kernel_ms"] * 1e-3)
                             / 1e12 / FP64_PEAK_TFLOPS} if sustained else {}),
                         "transport_kernel": {"bound": "hbm", "achieved_gbs": achieved, "peak_gbs": peak,

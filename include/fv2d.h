@@ -75,12 +75,15 @@ typedef enum { FV2D_AOS = 0, FV2D_SOA = 1 } fv2d_layout;
                                         every neighbour re-derived, every face computed twice.
                                         Same bits, ~2.5x the FP64 work; kept as a baseline. */
 #define FV2D_FLAG_SPLIT_SOURCE 0x2u /* spray: source as a separate pass after transport
-                                        (the default; kept for compatibility) */
+                                        (the only mode; accepted for compatibility) */
 #define FV2D_FLAG_ONE_CELL 0x4u     /* fused kernel with one cell per lane instead of the
                                         default two-cells-per-lane kernel (same bits) */
-#define FV2D_FLAG_FUSE_SOURCE 0x10u /* spray: apply the source in the transport pass's
-                                        epilogue (one pass, 96 B/cell less traffic; lower
-                                        occupancy for the FP64-bound Newton, slower on B200) */
+#define FV2D_FLAG_FUSE_SOURCE 0x10u /* reserved (removed): a one-pass spray step (flux + update +
+                                        source per cell) was built and measured slower than the
+                                        split source pass on B200 (2.38 vs 1.96 ms at 4096^2; the
+                                        source is issue-bound and the transport's instructions land
+                                        on that pipe).  fv2d_create returns
+                                        FV2D_E_ARG if it is set. */
 #define FV2D_FLAG_GRAPH 0x20u      /* replay each step from a CUDA graph captured once per
                                         ping-pong parity (re-captured when dt/mode change);
                                         single-process contexts only */

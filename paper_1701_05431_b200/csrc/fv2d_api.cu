@@ -201,7 +201,6 @@ struct fv2d_ctx {
   int sms = 0;               // multiprocessors of cfg.device
   int slots = 0;             // resident CTAs of the marching step kernel (sms x occupancy)
   int src_slots = 0;         // resident CTAs of the spray source pass (its persistent grid)
-  int fused_slots = 0;       // resident CTAs of the fused spray step (its persistent grid)
   bool guard_done = false;   // S:440 guard passed since the last set_state
   long long steps = 0;
   long long launches = 0;
@@ -424,7 +423,6 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.bad_cell = ctx->dscal + 3;
   a.done = ctx->done;
   a.fused_finalize = ctx->use_nccl ? 0 : 1;
-  a.fuse_source = (ctx->cfg.system == FV2D_SPRAY && (ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE)) ? 1 : 0;
   if (ctx->trig) {  // tables over the global mesh; x tables offset to this block
     a.sx_tab = ctx->trig + ctx->col0;
     a.cx_tab = ctx->trig + ctx->gnx + ctx->col0;
@@ -477,43 +475,6 @@ void launch_pair(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
   else launch_pair_x<Sys, D, XM_CLAMP>(ctx, a, grid);
 }
 
-// The fused spray step (spray_fused_step_kernel): persistent grid of
-// fused_slots 64-thread CTAs, i.e. 2 x fused_slots independent warps, each
-// marching items of 32 columns x one strip of rows.  Strip height per row
-// range: minimise waves x (rows + halo/8) over 2..64 rows -- a halo row costs a
-// load and a derive, an owned row also the Newton reconstruction (~30x more).
-int pick_rps_fused(const fv2d_ctx* ctx, int ncols, int nrows) {
-  const long long C = (ncols + 31) / 32;
-  const long long warps = 2LL * std::max(1, ctx->fused_slots);
-  long long best = -1;
-  int best_rps = std::min(nrows, 64);
-  for (int rps = 2; rps <= 64; ++rps) {
-    const long long S = (nrows + rps - 1) / rps;
-    const long long cost = ((C * S + warps - 1) / warps) * (8LL * rps + 2);
-    if (best < 0 || cost < best) {
-      best = cost;
-      best_rps = rps;
-    }
-    if (rps >= nrows) break;
-  }
-  return std::max(1, std::min(best_rps, nrows));
-}
-
-void launch_fused(const fv2d_ctx* ctx, const StepArgs& a0) {
-  StepArgs a = a0;
-  const int ncols = a.col_hi - a.col_lo;
-  set_ranges(a, a.row_lo[0], a.row_hi[0], pick_rps_fused(ctx, ncols, a.row_hi[0] - a.row_lo[0]), a.row_lo[1],
-             a.nranges > 1 ? a.row_hi[1] : a.row_lo[1],
-             a.nranges > 1 ? pick_rps_fused(ctx, ncols, a.row_hi[1] - a.row_lo[1]) : 1);
-  const long long items = (long long)total_strips(a) * ((ncols + 31) / 32) * ctx->nslabs;
-  const long long ctas = std::max<long long>(1, std::min<long long>((items + 1) / 2, std::max(1, ctx->fused_slots)));
-  const dim3 grid((unsigned)ctas);
-  cudaStream_t ls = ctx->launch_stream;
-  if (ctx->xg) spray_fused_step_kernel<XM_GHOST><<<grid, kSrcThreads, 0, ls>>>(a);
-  else if (ctx->cfg.bc_x == FV2D_BC_PERIODIC) spray_fused_step_kernel<XM_PERIODIC><<<grid, kSrcThreads, 0, ls>>>(a);
-  else spray_fused_step_kernel<XM_CLAMP><<<grid, kSrcThreads, 0, ls>>>(a);
-}
-
 template <class Sys>
 struct LaunchStep {
   static void run(const fv2d_ctx* ctx, const StepArgs& a) {
@@ -523,12 +484,8 @@ struct LaunchStep {
     } else {
       constexpr int D = 4;
       const bool xper = ctx->cfg.bc_x == FV2D_BC_PERIODIC && !ctx->xg;
-      // spray (nVar 6) uses the one-cell kernel: its fused source needs the registers
+      // spray (nVar 6) uses the one-cell kernel: two cells of 6 variables per lane would spill
       if constexpr (Sys::NV == 6) {
-        if (a.fuse_source) {  // transport + source in one pass
-          launch_fused(ctx, a);
-          return;
-        }
         const int cols = 30 * kWarps;
         dim3 grid((a.col_hi - a.col_lo + cols - 1) / cols, total_strips(a), ctx->nslabs);
         cudaStream_t ls = ctx->launch_stream;
@@ -626,10 +583,6 @@ cudaError_t query_geometry(fv2d_ctx* ctx) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&src, spray_source_step_kernel, kSrcThreads, 0);
     if (e != cudaSuccess) return e;
     ctx->src_slots = ctx->sms * std::max(1, src);
-    int fu = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fu, spray_fused_step_kernel<XM_PERIODIC>, kSrcThreads, 0);
-    if (e != cudaSuccess) return e;
-    ctx->fused_slots = ctx->sms * std::max(1, fu);
   }
   return cudaSuccess;
 }
@@ -685,11 +638,6 @@ struct Preload {
     t(touch(fv_step_kernel<Sys, true, true, kWarps, 4>));
     t(touch(fv_step_kernel<Sys, false, false, kWarps, 4>));
     t(touch(fv_step_kernel<Sys, false, true, kWarps, 4>));
-    if constexpr (Sys::NV == 6) {
-      t(touch(spray_fused_step_kernel<XM_CLAMP>));
-      t(touch(spray_fused_step_kernel<XM_PERIODIC>));
-      t(touch(spray_fused_step_kernel<XM_GHOST>));
-    }
     t(touch(finalize_kernel));
     t(touch(peer_collective_kernel));
     t(touch(promote_pending_kernel));
@@ -994,6 +942,9 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   if (c.system == FV2D_ADVECTION && (c.bc_x == FV2D_BC_WALL || c.bc_y == FV2D_BC_WALL)) return FV2D_E_ARG;
   if (c.system == FV2D_EULER && !(c.param[0] > 1.0)) return FV2D_E_ARG;
   if (c.system == FV2D_SPRAY && !(c.param[1] > 0.0)) return FV2D_E_ARG;
+  // FV2D_FLAG_FUSE_SOURCE (a one-pass spray step) was measured slower than the
+  // split source pass on B200 and removed; the bit stays reserved
+  if (c.flags & FV2D_FLAG_FUSE_SOURCE) return FV2D_E_ARG;
   for (int k = 0; k < 4; ++k)
     if (c.reserved[k] != 0) return FV2D_E_ARG;
   // 2-D rank blocks (nranks_x > 1): nranks_x x (nranks/nranks_x) blocks
@@ -1383,7 +1334,7 @@ static void spray_source_dt_kernel_launch(fv2d_ctx* ctx, const StepArgs& a, dim3
 // caller's stream, or the capture stream while recording a CUDA graph).
 static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, double cfl, cudaEvent_t e1) {
   fv2d_status st = FV2D_OK;
-  const bool split = ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE);
+  const bool split = ctx->cfg.system == FV2D_SPRAY;
   const bool tiled = ctx->tiles_x * ctx->tiles_y > 1 && !(ctx->cfg.flags & FV2D_FLAG_NAIVE);
   StepArgs a = make_args(ctx, p);
   a.adaptive = adaptive;
@@ -1404,7 +1355,6 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
   }
   StepArgs at = a;  // transport pass
   if (split) {
-    at.fuse_source = 0;
     at.fused_finalize = 0;  // the source pass ends the step
     at.no_smax = 1;         // adaptive: smax of the post-source state comes from the source pass
   }
@@ -1550,7 +1500,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
     ctx->dt_valid = adaptive != 0;
     ctx->dt_cfl = cfl;
   }
-  const bool split = ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE);
+  const bool split = ctx->cfg.system == FV2D_SPRAY;
   const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl && !ctx->peer;
   for (int32_t k = 0; k < nsteps; ++k) {
     const int p = cur_parity(ctx);
@@ -1577,10 +1527,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
       st = issue_step(ctx, p, adaptive, dt, cfl, e1);
       if (st) return st;
     }
-    // the source pass, or the fused spray step, wrote this step's multipliers
-    // (the paper-style kernel's fused source starts every Newton cold)
-    if (split || (ctx->cfg.system == FV2D_SPRAY && !(ctx->cfg.flags & FV2D_FLAG_NAIVE)))
-      ctx->lam_hist = std::min(2, ctx->lam_hist + 1);
+    if (split) ctx->lam_hist = std::min(2, ctx->lam_hist + 1);  // the source pass wrote lambda_{n+1}
     ctx->steps += 1;
   }
   return FV2D_OK;
@@ -1732,7 +1679,6 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   a.fused_finalize = 0;
   const bool spray = ctx->cfg.system == FV2D_SPRAY;  // split source pass per band after its transport
   StepArgs at = a;
-  at.fuse_source = 0;
   at.no_smax = 1;
   StepArgs hf = make_args(ctx, 1);  // halo targets of parity 0 (as after_set_state)
   hf.slab[0].in = row_ptr(ctx, 0, 0, 0);
@@ -1814,7 +1760,7 @@ fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_ou
   // (the S:440 guard), so only transport systems pipeline the upload
   const bool pipelined = layout == FV2D_AOS && nsteps >= 1 && ctx->cfg.nranks == 1 && ctx->nslabs == 1 &&
                          ctx->cfg.system != FV2D_SPRAY &&
-                         !ctx->use_nccl && !ctx->peer && !(ctx->cfg.flags & FV2D_FLAG_FUSE_SOURCE) &&
+                         !ctx->use_nccl && !ctx->peer &&
                          !(ctx->cfg.flags & FV2D_FLAG_NAIVE) && ctx->H >= 128;
   fv2d_status st;
   if (pipelined) {

@@ -59,6 +59,9 @@ def test_create_validates_before_touching_the_device():
     L.fv2d_config_default(C.byref(cfg), 8, 8, fv2d.ADVECTION)
     cfg.bc_x = fv2d.BC_WALL             # wall undefined for advection
     assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
+    L.fv2d_config_default(C.byref(cfg), 8, 8, fv2d.SPRAY)
+    cfg.flags = fv2d.FLAG_FUSE_SOURCE       # removed one-pass spray step (reserved bit)
+    assert L.fv2d_create(C.byref(cfg), None, None, C.byref(h)) == fv2d.E_ARG
     assert L.fv2d_step(None, 1e-3, 1) == fv2d.E_ARG
     assert L.fv2d_destroy(None) == fv2d.OK
 

@@ -136,7 +136,7 @@ def test_block_decomposition_advection_fixed_dt():
     assert np.array_equal(W, ref.W)
 
 
-@pytest.mark.parametrize("flags", [0, fv2d.FLAG_FUSE_SOURCE])
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_NAIVE])
 def test_block_decomposition_spray(flags):
     """Spray: tolerance parity (device exp/sincospi vs glibc); the source's
     Taylor-Green drag uses the block's global cell centres."""

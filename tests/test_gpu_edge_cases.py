@@ -38,7 +38,7 @@ def spray_case(n, K=1.0):
 
 
 # ------------------------------------------------------------ S:440 guard
-@pytest.mark.parametrize("flags", [0, fv2d.FLAG_FUSE_SOURCE])
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_NAIVE])
 def test_spray_guard_fixed_dt(flags):
     """dt*K > 0.1*min(m3/m1) is rejected at startup with E_ARG, the
     argmin cell and value of the oracle, W^0 untouched and no step taken; a
@@ -112,7 +112,7 @@ def test_spray_guard_after_cfl_precedence():
 
 
 # ------------------------------------------------------------ E_RECON
-@pytest.mark.parametrize("flags", [0, fv2d.FLAG_FUSE_SOURCE])
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_NAIVE])
 def test_nonrealizable_cell_latches_recon(flags):
     """A cell whose moments violate m1^2 <= m0 m2 (no positive measure, S:402
     precondition): the source step's reconstruction fails there; both sides

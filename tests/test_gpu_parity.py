@@ -212,7 +212,7 @@ def spray_case(n):
     return cfg, W0, 0.5 * (1.0 / n) / s0     # R17
 
 
-@pytest.mark.parametrize("flags", [0, fv2d.FLAG_FUSE_SOURCE])
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_NAIVE])
 def test_spray_per_step_and_trajectory(flags):
     """Source parity is tolerance-only (GPU exp/sincospi vs glibc): per step
     <= 1e-12 from the same W^k, after 20 steps <= 1e-10."""
@@ -236,10 +236,10 @@ def test_spray_apply_source_standalone():
     assert relerr(W, ref) <= 1e-12
 
 
-@pytest.mark.parametrize("flags", [0, fv2d.FLAG_FUSE_SOURCE])
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_NAIVE])
 def test_spray_adaptive(flags):
     """Adaptive dt with the source: smax is reduced on the post-source state
-    (split: in the source pass's epilogue; fused: in the step epilogue)."""
+    (in the source pass's epilogue); both transport kernels."""
     cfg, W0, _ = spray_case(40)
     ref = O.run(cfg, W0, 10, O.ADAPTIVE, 0.5)
     W, log = gpu_run(cfg, W0, 10, O.ADAPTIVE, 0.5, flags=flags)

@@ -1,7 +1,7 @@
 """Device-time throughput of every BASELINE config on one GPU (JSONL to stdout).
 
 c1 advection 64^2, c2 Euler 1024^2 (Lax-Liu 3), c3 Euler 16384^2 (also in bench.py),
-c4 spray 4096^2 (Taylor-Green, fused and split source), c5 Euler 8192^2 per GPU, plus
+c4 spray 4096^2 (Taylor-Green), c5 Euler 8192^2 per GPU, plus
 the fused kernel variants (pair / one-cell / paper-style naive) and adaptive dt.
 Timing: CUDA events on the library stream around K steps after W warm-up steps.
 """
@@ -86,9 +86,7 @@ if __name__ == "__main__":
         n = 4096
         W = inputs.spray_taylor_green(n, n)
         fd = lambda smax: 0.5 * (1.0 / n) / smax
-        run("c4_spray_4096_split", fv2d.SPRAY, n, W, 10, 3, param=(1.0, 1.0), fixed_dt=fd)
-        run("c4_spray_4096_fused", fv2d.SPRAY, n, W, 10, 3, param=(1.0, 1.0), fixed_dt=fd,
-            flags=fv2d.FLAG_FUSE_SOURCE)
+        run("c4_spray_4096", fv2d.SPRAY, n, W, 10, 3, param=(1.0, 1.0), fixed_dt=fd)
     if want("paper"):
         # the paper's own workloads (context: PAPER.md 889-900 Euler 16384^2 x 50 iterations in
         # 61 s on 4 CPU workers + 4 GPUs; 1063-1071 spray 200^2 x 100 iterations in 5.81 s)

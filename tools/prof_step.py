@@ -14,12 +14,10 @@ ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--system", default="euler")
 ap.add_argument("--naive", action="store_true")
 ap.add_argument("--adaptive", action="store_true")
-ap.add_argument("--fuse", action="store_true")
 ap.add_argument("--one-cell", action="store_true")
 a = ap.parse_args()
 n = a.n
-flags = (fv2d.FLAG_NAIVE if a.naive else 0) | (fv2d.FLAG_FUSE_SOURCE if a.fuse else 0) | \
-    (fv2d.FLAG_ONE_CELL if a.one_cell else 0)
+flags = (fv2d.FLAG_NAIVE if a.naive else 0) | (fv2d.FLAG_ONE_CELL if a.one_cell else 0)
 if a.system == "euler":
     W0 = np.empty((n, n, 4))
     for j in range(0, n, 1024):

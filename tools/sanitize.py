@@ -15,7 +15,7 @@ cases = [
     dict(nx=125, ny=64, system=fv2d.EULER, param=(1.4,), nslabs=4, W=inputs.euler_random(125, 64, seed=7)),
     dict(nx=64, ny=64, system=fv2d.ADVECTION, param=(1.0, 0.5), W=inputs.advection_dyadic(64, 64)),
     dict(nx=33, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), W=inputs.spray_taylor_green(33, 32)),
-    dict(nx=33, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), flags=fv2d.FLAG_FUSE_SOURCE,
+    dict(nx=33, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), flags=fv2d.FLAG_NAIVE,
          W=inputs.spray_taylor_green(33, 32)),
     dict(nx=100, ny=40, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_NAIVE, W=inputs.euler_random(100, 40)),
     dict(nx=100, ny=40, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_ONE_CELL, W=inputs.euler_random(100, 40)),
