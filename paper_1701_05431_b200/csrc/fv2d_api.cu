@@ -170,11 +170,11 @@ struct fv2d_ctx {
   unsigned long long* newton = nullptr;
   double* trig = nullptr;  // sx[nx] cx[nx] sy[ny] cy[ny]
   // spray: Newton warm start, two caches of nslabs x H x 4 x pitch: the pass
-  // reading state parity p reads lambda_n from lam_buf[p] and lambda_{n-1} from
-  // lam_buf[1-p] and writes lambda_{n+1} over lambda_{n-1} (a CUDA graph is
-  // captured per parity, and recaptured when lam_hist changes)
-  double* lam_buf[2] = {nullptr, nullptr};
-  int lam_hist = 0;  // valid history entries: 0 (cold start), 1 (lambda_n), 2 (and lambda_{n-1})
+  // the multipliers after step n are in lam_buf[n % 3]; the kernels select the
+  // levels from the device step counter (StepArgs::lam3), so a CUDA graph
+  // captured per parity stays valid (it is recaptured when lam_hist changes)
+  double* lam_buf[3] = {nullptr, nullptr, nullptr};
+  int lam_hist = 0;  // valid levels: 0 (cold start), 1 (lambda_n), 2 (+lambda_{n-1}), 3 (+lambda_{n-2})
   ncclComm_t comm = nullptr;
   bool use_nccl = false;  // nranks > 1, or FV2D_FLAG_NCCL_LOOPBACK (self exchange on 1 rank)
   // FV2D_FLAG_PEER_HALO: halo rows and the CFL max-all-reduce through peer memory
@@ -433,10 +433,8 @@ StepArgs make_args(const fv2d_ctx* ctx, int p) {
   a.step_dev = reinterpret_cast<long long*>(ctx->dscal + 6);
   a.col_lo = 0;
   a.col_hi = ctx->nx;
-  a.lam_in = ctx->lam_buf[p];
-  a.lam_out = ctx->lam_buf[q];
-  a.lam_old = ctx->lam_hist >= 2 ? ctx->lam_buf[q] : nullptr;
-  a.lam_valid = ctx->lam_hist >= 1 ? 1 : 0;
+  for (int k = 0; k < 3; ++k) a.lam3[k] = ctx->lam_buf[k];
+  a.lam_hist = ctx->lam_hist;
   a.peer_fence = ctx->peer ? 1 : 0;
   if (ctx->peer) a.fused_finalize = 0;
   a.xghost = ctx->xg ? 1 : 0;
@@ -1527,7 +1525,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
       st = issue_step(ctx, p, adaptive, dt, cfl, e1);
       if (st) return st;
     }
-    if (split) ctx->lam_hist = std::min(2, ctx->lam_hist + 1);  // the source pass wrote lambda_{n+1}
+    if (split) ctx->lam_hist = std::min(3, ctx->lam_hist + 1);  // the source pass wrote lambda_{n+1}
     ctx->steps += 1;
   }
   return FV2D_OK;
@@ -1742,7 +1740,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   CK(cudaStreamWaitEvent(ctx->stream, ev_start, 0));
   ctx->has_state = true;
   ctx->dt_valid = false;
-  ctx->lam_hist = spray ? 1 : 0;  // lambda_1 of every cell is in lam_buf[1]
+  ctx->lam_hist = spray ? 1 : 0;  // lambda_1 of every cell is in lam_buf[1 % 3]
   ctx->err.clear();
   ctx->err_step = ctx->err_cell = -1;
   ctx->steps = 1;
@@ -1813,11 +1811,9 @@ fv2d_status fv2d_apply_source(fv2d_ctx* ctx, double dt) {
   StepArgs b = make_args(ctx, 1 - p);
   for (int s = 0; s < ctx->nslabs; ++s) b.slab[s].out = row_ptr(ctx, s, p, 0);
   b.step = ctx->steps;
-  // the multipliers of the current state W (parity p) are in lam_buf[p]: warm
-  // start from them, no extrapolation, write back in place (history broken)
-  b.lam_in = ctx->lam_buf[p];
-  b.lam_out = ctx->lam_buf[p];
-  b.lam_old = nullptr;
+  // the multipliers of the current state W^n are in lam_buf[n % 3]: warm start
+  // from them, no extrapolation, write back in place (history broken)
+  b.lam_inplace = 1;
   spray_source_kernel<<<src_grid(ctx, ctx->H, ctx->nslabs), kSrcThreads, 0, ctx->stream>>>(b, dt, 0);
   CKL();
   ctx->lam_hist = 1;
