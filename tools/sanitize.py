@@ -17,6 +17,11 @@ cases = [
     dict(nx=33, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), W=inputs.spray_taylor_green(33, 32)),
     dict(nx=33, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), flags=fv2d.FLAG_NAIVE,
          W=inputs.spray_taylor_green(33, 32)),
+    # spray with two slabs and with CUDA-graph replay (the three multiplier levels
+    # rotate with the device step counter)
+    dict(nx=40, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), nslabs=2, W=inputs.spray_taylor_green(40, 32)),
+    dict(nx=40, ny=32, system=fv2d.SPRAY, param=(1.0, 1.0), flags=fv2d.FLAG_GRAPH,
+         W=inputs.spray_taylor_green(40, 32)),
     dict(nx=100, ny=40, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_NAIVE, W=inputs.euler_random(100, 40)),
     dict(nx=100, ny=40, system=fv2d.EULER, param=(1.4,), flags=fv2d.FLAG_ONE_CELL, W=inputs.euler_random(100, 40)),
     dict(nx=130, ny=60, system=fv2d.EULER, param=(1.4,), tiles=(3, 4), W=inputs.euler_random(130, 60)),
