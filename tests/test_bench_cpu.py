@@ -126,6 +126,7 @@ def test_bench_spray_workload_fp64_roofline():
     rf = d["roofline"]
     assert rf["bound"] == "alu" and rf["unit"] == "TFLOP/s" and 0 < rf["frac"] < 1
     assert rf["arithmetic_intensity_flop_per_byte"] > 5.7        # above the FP64 ridge
+    assert 0 < rf["fp64_instr_frac"] < 1 and rf["fp64_instr_per_cell"] > 0   # the pipe's instruction rate
     assert rf["transport_kernel"]["bound"] == "hbm"
     assert d["value"] > 1e9 and d["e2e"]["value"] > 0 and d["cpu_baseline"]["value"] > 0
     assert 0.5 < d["config"]["newton_iters_per_cell_step"] < 3

@@ -749,3 +749,39 @@ def test_create_destroy_releases_device_memory():
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 64 << 20, (free0, free1)
+
+
+def _random_spray_case(seed):
+    rng = np.random.default_rng(5000 + seed)
+    nslabs = int(rng.choice([1, 1, 2, 3]))
+    ny = int(rng.integers(2, 24)) * nslabs
+    nx = int(rng.integers(3, 140))
+    W0 = inputs.spray_taylor_green(nx, ny)
+    bcs = [O.BC_PERIODIC, O.BC_DIRICHLET, O.BC_WALL]
+    bc_x, bc_y = int(rng.choice(bcs)), int(rng.choice(bcs))
+    x1, y1 = float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 2.0))
+    dirichlet = tuple(W0[int(rng.integers(0, ny)), int(rng.integers(0, nx))])
+    flags = int(rng.choice([0, 0, fv2d.FLAG_NAIVE, fv2d.FLAG_GRAPH]))
+    tiles = (1, 1)
+    if flags != fv2d.FLAG_NAIVE and rng.random() < 0.3 and nx >= 8:
+        tiles = (int(rng.integers(1, min(4, nx // 2) + 1)), int(rng.integers(1, min(3, ny // nslabs) + 1)))
+    cfg = O.Config(nx=nx, ny=ny, system=O.SPRAY, param=(float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 2.0))),
+                   bc_x=bc_x, bc_y=bc_y, x1=x1, y1=y1, dirichlet=dirichlet)
+    s0, _ = O.smax(cfg, W0)
+    dt = 0.5 * min(x1 / nx, y1 / ny) / s0          # R17
+    return cfg, W0, dict(nslabs=nslabs, flags=flags, tiles=tiles), int(rng.integers(1, 9)), dt
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_randomized_spray_configurations(seed):
+    """The spray over random ragged meshes, domains, K and theta, boundary
+    conditions (periodic / Dirichlet / wall), slab counts, transport kernels,
+    tiles and graph replay: the source pass with its warm-start history (up to
+    three multiplier levels) stays within the north_star tolerance of the
+    cold-started oracle (<= 1e-12 after one step, <= 1e-10 after several)."""
+    cfg, W0, kw, nsteps, dt = _random_spray_case(seed)
+    ref = O.run(cfg, W0, nsteps, O.FIXED, dt, raise_on_error=False)
+    if ref.status != O.OK:
+        pytest.skip(f"oracle status {ref.status} for this random case")
+    W, _ = gpu_run(cfg, W0, nsteps, O.FIXED, dt, **kw)
+    assert relerr(W, ref.W) <= (1e-12 if nsteps == 1 else 1e-10), (cfg, kw)
