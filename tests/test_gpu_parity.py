@@ -586,13 +586,39 @@ def test_c4_full_size_4096_spray_sampled_rows():
         assert relerr(got, band[1:-1]) <= 1e-12
 
 
+def test_c4_full_size_steady_state_warm_start_sampled_rows():
+    """c4 at full size in its steady state: after 5 steps the source pass starts
+    Newton from the second-order extrapolation of three multiplier levels and
+    takes order-2 moment-space trial points; step 6 is compared
+    on sampled row bands with the oracle's cold-started step from the GPU's own
+    W^5 (stencil-local transport, cell-local source): <= 1e-12."""
+    n = 4096
+    cfg = O.Config(nx=n, ny=n, system=O.SPRAY, param=(1.0, 1.0))
+    W0 = inputs.spray_taylor_green(n, n)
+    s0, _ = O.smax(cfg, W0)
+    dt = 0.5 * (1.0 / n) / s0
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        s.step(dt, 5)
+        W5 = s.get_state()
+        s.step(dt, 1)
+        W6 = s.get_state()
+    for j0 in (0, 2047, 4090):
+        rows = [r % n for r in range(j0 - 1, j0 + 7)]
+        bcfg = O.Config(nx=n, ny=len(rows), system=O.SPRAY, param=(1.0, 1.0), y0=(j0 - 1) / n,
+                        y1=(j0 - 1 + len(rows)) / n)
+        band = O.transport_step(bcfg, W5[rows], dt)
+        band, _ = O.source_step(bcfg, band, dt)
+        got = W6[[r % n for r in range(j0, j0 + 6)]]
+        assert relerr(got, band[1:-1]) <= 1e-12
+
+
 @pytest.mark.parametrize("p0", [1.0, 1e-7])
 def test_adaptive_smax_near_ties_and_high_mach(p0):
-    """The adaptive epilogue skips cells that provably cannot raise the running
-    smax (Euler.below).  Adversarial input: a uniform state whose
-    cells differ only in the last bits (near-ties everywhere), at low and at
-    extreme Mach number (p = 1e-7: cancellation in p = gm1 (E - ke)).  The dt
-    sequence must still equal the oracle's exactly."""
+    """Adversarial input for the adaptive dt: a uniform state whose cells differ
+    only in the last bits (near-ties everywhere), at low and at extreme Mach
+    number (p = 1e-7: cancellation in p = gm1 (E - ke)).  The dt sequence must
+    still equal the oracle's exactly."""
     nx, ny = 256, 128
     rng = np.random.default_rng(11)
     rho, u, v = 1.0, 0.3, -0.2
