@@ -66,7 +66,9 @@ bool load_nccl() {
 
 // ------------------------------------------------------------------ GL-24 table
 // Gauss-Legendre nodes/weights on [0,1] by Newton's method on P_24 in long
-// double; uploaded once to constant memory.
+// double; uploaded once to constant memory as 2 w_q t_q^k (the
+// factor 2 of the moments folded into the weights: scaling by 2 is exact, so
+// every partial sum is exactly twice the unscaled one).
 void gl24_table(double t[24], double wt[24][kGLW]) {
   const int n = 24;
   for (int k = 0; k < n; ++k) {
@@ -97,7 +99,7 @@ void gl24_table(double t[24], double wt[24][kGLW]) {
     const double wq = (double)(w / 2);
     double tp = 1.0;
     for (int m = 0; m < kGLW; ++m) {
-      wt[q][m] = wq * tp;
+      wt[q][m] = 2.0 * (wq * tp);  // the moments' factor 2, folded in (exact: a power of two)
       tp = tp * t[q];
     }
   }
