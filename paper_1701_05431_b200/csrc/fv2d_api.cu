@@ -16,6 +16,8 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <type_traits>
+#include <vector>
 #include <vector>
 
 #include <nccl.h>
@@ -206,6 +208,25 @@ struct fv2d_ctx {
   bool guard_done = false;   // S:440 guard passed since the last set_state
   long long steps = 0;
   long long launches = 0;
+  // Branch-free division / square root in the Euler pair kernel (FAST, adaptive
+  // dt only): used by single-rank contexts (no NCCL or peer path) at the default ring depth, with
+  // an in-range Dirichlet state and no snapshot taken.  Steps are journaled
+  // until a status read finds nothing latched; a latched E_NONFINITE at a FAST
+  // step k (possibly an operand outside the fast range) is answered by
+  // recover_fast: the device state of "step k not taken" is restored (W^k is
+  // intact in its ping-pong buffer, later steps were no-ops) and steps k.. are
+  // re-run with the exact kernels, so results and errors are the exact ones.
+  bool fast_ok = false;
+  bool force_exact = false;  // fv2d_step_host: exact kernels
+  bool snap_used = false;
+  struct StepRec {
+    int adaptive;
+    double dt, cfl;
+    bool fast;
+  };
+  std::vector<StepRec> journal;  // journal[i] = step steps - journal.size() + i
+  int graph_fast = -1;
+  long long recoveries = 0;  // recover_fast re-runs (stats)
   // profiling: event pairs around step-kernel launches
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -219,6 +240,10 @@ struct fv2d_ctx {
   long long err_step = -1, err_cell = -1;
   double err_value = NAN;
 };
+
+extern "C" {
+static fv2d_status recover_fast(fv2d_ctx* ctx, unsigned long long st, bool* redone);
+}
 
 namespace {
 
@@ -455,15 +480,29 @@ void dispatch(int system, Args&&... args) {
   }
 }
 
-template <class Sys, int D, int XM, bool ADAPT>
+template <class Sys, int D, int XM, bool ADAPT, bool FAST = false>
 void launch_pair_1(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
   // (the dynamic shared-memory opt-in was set once at fv2d_create: preload_kernels)
   const int smem = kWarps * D * Sys::NV * 64 * (int)sizeof(double);
-  fv_step_pair_kernel<Sys, XM, ADAPT, kWarps, D><<<grid, kWarps * 32, smem, ctx->launch_stream>>>(a);
+  fv_step_pair_kernel<Sys, XM, ADAPT, kWarps, D, FAST><<<grid, kWarps * 32, smem, ctx->launch_stream>>>(a);
 }
+
+// The branch-free division / square root variant exists for Euler's adaptive
+// instantiation at the default ring depth: there it removes the second
+// derive's branches (0.87 -> 0.80 ms per 8192^2 step, adaptive within 0-5% of
+// fixed dt; profiles/r2s3_fastdiv_*.jsonl); the fixed-dt kernel does not gain
+// from it (it spills 8-16 B and ran 0.5% slower), so fixed dt stays exact.
+template <class Sys, int D>
+constexpr bool kHasFast = std::is_same<Sys, Euler>::value && D == 4;
 
 template <class Sys, int D, int XM>
 void launch_pair_x(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
+  if constexpr (kHasFast<Sys, D>) {
+    if (a.fast && a.adaptive) {
+      launch_pair_1<Sys, D, XM, true, true>(ctx, a, grid);
+      return;
+    }
+  }
   if (a.adaptive) launch_pair_1<Sys, D, XM, true>(ctx, a, grid);
   else launch_pair_1<Sys, D, XM, false>(ctx, a, grid);
 }
@@ -612,6 +651,11 @@ cudaError_t pair_attrs_x() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaError_t e2 = cudaFuncSetAttribute(fv_step_pair_kernel<Sys, XM, true, kWarps, D>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if constexpr (kHasFast<Sys, D>) {
+    cudaError_t e3 = cudaFuncSetAttribute(fv_step_pair_kernel<Sys, XM, true, kWarps, D, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e2 == cudaSuccess) e2 = e3;
+  }
   return e != cudaSuccess ? e : e2;
 }
 template <class Sys, int D>
@@ -761,7 +805,16 @@ fv2d_status d2h_words(fv2d_ctx* ctx, unsigned long long* dst, const unsigned lon
 }
 
 fv2d_status read_status(fv2d_ctx* ctx, unsigned long long* st_out) {
-  return d2h_words(ctx, st_out, ctx->dscal + 2, 1);
+  fv2d_status s0 = d2h_words(ctx, st_out, ctx->dscal + 2, 1);
+  if (s0 || ctx->journal.empty()) return s0;
+  if (*st_out == 0) {  // every journaled step completed without a latched error
+    ctx->journal.clear();
+    return FV2D_OK;
+  }
+  bool redone = false;
+  s0 = recover_fast(ctx, *st_out, &redone);
+  if (s0) return s0;
+  return redone ? read_status(ctx, st_out) : FV2D_OK;
 }
 
 // Translate a latched status word into an error code + description.
@@ -989,6 +1042,22 @@ fv2d_status fv2d_create(const fv2d_config* cfg_in, const uint8_t* nccl_id, void*
   ctx->H = (int)H;
   ctx->pitch = (nxl + ctx->xoff + (xg ? 1 : 0) + 31) / 32 * 32;
   if (const char* e = getenv("FV2D_RING_DEPTH")) ctx->ring_depth = atoi(e);  // tuning knob
+  {
+    // FAST pair kernel (see fv2d_ctx::fast_ok): single rank, default kernel and
+    // ring, and a Dirichlet state (never an output cell, so never checked by the
+    // kernel) whose derive stays inside the fast range: 1e-300 < rho < 1e300,
+    // p > 0 and 1e-300 < gamma p / rho < 1e300
+    bool dir_ok = true;
+    if (c.system == FV2D_EULER && (c.bc_x == FV2D_BC_DIRICHLET || c.bc_y == FV2D_BC_DIRICHLET)) {
+      const double rho = c.dirichlet[0], mx = c.dirichlet[1], my = c.dirichlet[2], E = c.dirichlet[3];
+      const double g = c.param[0], inv = 1.0 / rho, p = (g - 1.0) * (E - 0.5 * (mx * mx + my * my) * inv),
+                   X = g * p * inv;
+      dir_ok = rho > 1e-300 && rho < 1e300 && p > 0.0 && X > 1e-300 && X < 1e300 && std::isfinite(E);
+    }
+    const char* ex = getenv("FV2D_EXACT_DIV");  // 1: never the FAST kernel (A/B knob)
+    ctx->fast_ok = c.system == FV2D_EULER && !use_nccl && !peer && c.nranks <= 1 && ctx->ring_depth == 4 &&
+                   !(c.flags & (FV2D_FLAG_NAIVE | FV2D_FLAG_ONE_CELL)) && dir_ok && !(ex && atoi(ex) == 1);
+  }
   ctx->rs = (long long)ctx->pitch * nv;
   ctx->nslabs = c.nslabs;
   ctx->G = py * c.nslabs;
@@ -1152,6 +1221,7 @@ static fv2d_status after_set_state(fv2d_ctx* ctx) {
   ctx->dt_valid = false;
   ctx->guard_done = false;
   ctx->lam_hist = 0;
+  ctx->journal.clear();
   ctx->err.clear();
   ctx->err_step = ctx->err_cell = -1;
   return FV2D_OK;
@@ -1271,6 +1341,11 @@ fv2d_status fv2d_check_dt(fv2d_ctx* ctx, double dt, double* smax) {
   if (!ctx || !(dt > 0.0)) return FV2D_E_ARG;
   if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
   CK(cudaSetDevice(ctx->cfg.device));
+  if (!ctx->journal.empty()) {
+    unsigned long long st0;
+    fv2d_status s0 = read_status(ctx, &st0);
+    if (s0) return s0;
+  }
   double s;
   unsigned long long pend;
   fv2d_status s0 = reduce_current(ctx, &s, &pend);
@@ -1332,12 +1407,14 @@ static void spray_source_dt_kernel_launch(fv2d_ctx* ctx, const StepArgs& a, dim3
 
 // The launches of one time step reading parity p, on ctx->launch_stream (the
 // caller's stream, or the capture stream while recording a CUDA graph).
-static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, double cfl, cudaEvent_t e1) {
+static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, double cfl, cudaEvent_t e1,
+                              bool fast) {
   fv2d_status st = FV2D_OK;
   const bool split = ctx->cfg.system == FV2D_SPRAY;
   const bool tiled = ctx->tiles_x * ctx->tiles_y > 1 && !(ctx->cfg.flags & FV2D_FLAG_NAIVE);
   StepArgs a = make_args(ctx, p);
   a.adaptive = adaptive;
+  a.fast = fast ? 1 : 0;
   a.dt = dt;
   a.cfl = cfl;
   a.step = ctx->steps;
@@ -1464,7 +1541,7 @@ static fv2d_status issue_step(fv2d_ctx* ctx, int p, int adaptive, double dt, dou
 }
 
 // Record one step per parity into CUDA graphs (FV2D_FLAG_GRAPH).
-static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double cfl) {
+static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double cfl, bool fast) {
   if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
   for (int p = 0; p < 2; ++p) {
     if (ctx->graph[p]) {
@@ -1474,7 +1551,7 @@ static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double
     cudaGraph_t g;
     ctx->launch_stream = ctx->cap_stream;
     CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
-    fv2d_status st = issue_step(ctx, p, adaptive, dt, cfl, nullptr);
+    fv2d_status st = issue_step(ctx, p, adaptive, dt, cfl, nullptr, fast);
     cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
     ctx->launch_stream = ctx->stream;
     if (st) return st;
@@ -1483,6 +1560,7 @@ static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double
     CK(cudaGraphDestroy(g));
   }
   ctx->graph_ready = true;
+  ctx->graph_fast = fast ? 1 : 0;
   ctx->graph_adaptive = adaptive;
   ctx->graph_dt = dt;
   ctx->graph_cfl = cfl;
@@ -1491,7 +1569,8 @@ static fv2d_status capture_graphs(fv2d_ctx* ctx, int adaptive, double dt, double
   return FV2D_OK;
 }
 
-static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double cfl, int32_t nsteps) {
+static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double cfl, int32_t nsteps,
+                                bool exact = false) {
   fv2d_status st = ensure_dt_log(ctx, ctx->steps + nsteps);
   if (st) return st;
   // dt_dev holds dt_{n} = (C*hmin)/smax(W^n) only after adaptive steps with
@@ -1502,6 +1581,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
   }
   const bool split = ctx->cfg.system == FV2D_SPRAY;
   const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl && !ctx->peer;
+  const bool fast = ctx->fast_ok && adaptive && !exact && !ctx->force_exact && !ctx->snap_used;
   for (int32_t k = 0; k < nsteps; ++k) {
     const int p = cur_parity(ctx);
     if (ctx->snap_parity == 1 - p) {  // this step writes the buffer a snapshot is reading
@@ -1516,20 +1596,62 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
     }
     if (use_graph) {
       if (!ctx->graph_ready || ctx->graph_adaptive != adaptive || ctx->graph_dt != dt || ctx->graph_cfl != cfl ||
-          ctx->graph_lam_hist != ctx->lam_hist || ctx->graph_dt_log != ctx->dt_log) {
-        st = capture_graphs(ctx, adaptive, dt, cfl);
+          ctx->graph_lam_hist != ctx->lam_hist || ctx->graph_dt_log != ctx->dt_log ||
+          ctx->graph_fast != (fast ? 1 : 0)) {
+        st = capture_graphs(ctx, adaptive, dt, cfl, fast);
         if (st) return st;
       }
       CK(cudaGraphLaunch(ctx->graph[p], ctx->stream));
       ctx->launches += 1;
       if (e1) CK(cudaEventRecord(e1, ctx->stream));
     } else {
-      st = issue_step(ctx, p, adaptive, dt, cfl, e1);
+      st = issue_step(ctx, p, adaptive, dt, cfl, e1, fast);
       if (st) return st;
     }
+    if (ctx->fast_ok) ctx->journal.push_back({adaptive, dt, cfl, fast});
     if (split) ctx->lam_hist = std::min(3, ctx->lam_hist + 1);  // the source pass wrote lambda_{n+1}
     ctx->steps += 1;
   }
+  return FV2D_OK;
+}
+
+// A latched E_NONFINITE at step k that ran the FAST pair kernel: restore the
+// device state of "step k not taken" (no latched status, accumulators clear,
+// step counter k, dt_dev = dt_k for an adaptive step -- the failing finalize
+// logged it before overwriting dt_dev) and re-run steps k .. steps-1 from the
+// journal with the exact kernels.  W^k is intact: step k wrote the other
+// ping-pong buffer and every later step returned at its status check.
+static fv2d_status recover_fast(fv2d_ctx* ctx, unsigned long long st, bool* redone) {
+  *redone = false;
+  const int code = (int)(st >> 56);
+  const long long k = (long long)(st & 0x00FFFFFFFFFFFFFFull);
+  const long long base = ctx->steps - (long long)ctx->journal.size();
+  if (code != ST_NONFINITE || k < base || k >= ctx->steps || !ctx->journal[k - base].fast) return FV2D_OK;
+  const std::vector<fv2d_ctx::StepRec> redo(ctx->journal.begin() + (k - base), ctx->journal.end());
+  ctx->journal.clear();
+  CK(cudaMemsetAsync(ctx->dscal, 0, 3 * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dscal + 3, 0xff, sizeof(unsigned long long), ctx->stream));
+  ctx->hpin[0] = (unsigned long long)k;
+  CK(cudaMemcpyAsync(ctx->dscal + 6, ctx->hpin, sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx->stream));
+  if (redo[0].adaptive)
+    CK(cudaMemcpyAsync(ctx->dt_dev, ctx->dt_log + k, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->steps = k;
+  ctx->recoveries += 1;
+  static const bool dbg = getenv("FV2D_DEBUG_FAST") != nullptr;
+  if (dbg)
+    fprintf(stderr, "[fv2d] fast-path recovery: steps %lld..%lld re-run with the exact kernels\n", k,
+            k + (long long)redo.size() - 1);
+  for (size_t i = 0; i < redo.size();) {
+    size_t j = i + 1;
+    while (j < redo.size() && redo[j].adaptive == redo[i].adaptive && redo[j].dt == redo[i].dt &&
+           redo[j].cfl == redo[i].cfl)
+      ++j;
+    fv2d_status s1 = launch_steps(ctx, redo[i].adaptive, redo[i].dt, redo[i].cfl, (int32_t)(j - i), true);
+    if (s1) return s1;
+    i = j;
+  }
+  *redone = true;
   return FV2D_OK;
 }
 
@@ -1619,10 +1741,11 @@ fv2d_status fv2d_step_adaptive(fv2d_ctx* ctx, double cfl, int32_t nsteps, double
   fv2d_status st = launch_steps(ctx, 1, 0.0, cfl, nsteps);
   if (st) return st;
   if (dt_log && nsteps > 0) {
-    CK(cudaMemcpyAsync(dt_log, ctx->dt_log + first, nsteps * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     unsigned long long s;
-    st = read_status(ctx, &s);
+    st = read_status(ctx, &s);  // (settles FAST steps first: recover_fast rewrites the log)
     if (st) return st;
+    CK(cudaMemcpyAsync(dt_log, ctx->dt_log + first, nsteps * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     if (s) return report(ctx, s);
   }
   return FV2D_OK;
@@ -1659,6 +1782,7 @@ static fv2d_status step_host_pipelined(fv2d_ctx* ctx, const double* host_in, dou
   auto hi = [&](int b) { return std::min(H, (b + 1) * R); };
   // W^0 -> parity 0, uploads in band order on the H2D stream (after prior work)
   ctx->steps = 0;
+  ctx->journal.clear();
   CK(cudaEventRecord(ev_start, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->h2d_stream, ev_start, 0));
   for (int b = 0; b < B; ++b) {
@@ -1756,6 +1880,13 @@ fv2d_status fv2d_step_host(fv2d_ctx* ctx, const double* host_in, double* host_ou
     return FV2D_E_ARG;
   if (ctx->peer && !ctx->peer_connected) return set_err(ctx, FV2D_E_STATE, "peer halo: call fv2d_peer_connect first");
   CK(cudaSetDevice(ctx->cfg.device));
+  // exact kernels throughout: the output is written as the steps complete, so
+  // there is no later point at which recover_fast could re-run one
+  struct ExactGuard {
+    fv2d_ctx* c;
+    ~ExactGuard() { c->force_exact = false; }
+  } exact_guard{ctx};
+  ctx->force_exact = true;
   // the spray's first step needs all of W^0 on the device before it starts
   // (the S:440 guard), so only transport systems pipeline the upload
   const bool pipelined = layout == FV2D_AOS && nsteps >= 1 && ctx->cfg.nranks == 1 && ctx->nslabs == 1 &&
@@ -1846,6 +1977,12 @@ fv2d_status fv2d_synchronize(fv2d_ctx* ctx) {
 fv2d_status fv2d_device_state(fv2d_ctx* ctx, int32_t slab, double** d_ptr, int64_t* pitch, int64_t* row_stride,
                               int32_t* ny_slab) {
   if (!ctx || slab < 0 || slab >= ctx->nslabs) return FV2D_E_ARG;
+  if (!ctx->journal.empty()) {  // settle the FAST steps first (recover_fast may re-run some)
+    CK(cudaSetDevice(ctx->cfg.device));
+    unsigned long long st;
+    fv2d_status s0 = read_status(ctx, &st);
+    if (s0) return s0;
+  }
   if (d_ptr) *d_ptr = row_ptr(ctx, slab, cur_parity(ctx), 0);
   if (pitch) *pitch = ctx->pitch;
   if (row_stride) *row_stride = ctx->rs;
@@ -1889,6 +2026,12 @@ fv2d_status fv2d_snapshot(fv2d_ctx* ctx, double* host, fv2d_layout layout) {
   if (!ctx || !host || (layout != FV2D_AOS && layout != FV2D_SOA)) return FV2D_E_ARG;
   if (!ctx->has_state) return set_err(ctx, FV2D_E_STATE, "no state set");
   CK(cudaSetDevice(ctx->cfg.device));
+  if (!ctx->journal.empty()) {  // settle the FAST steps; snapshots then run with exact kernels only
+    unsigned long long st;
+    fv2d_status s0 = read_status(ctx, &st);
+    if (s0) return s0;
+  }
+  ctx->snap_used = true;
   const int nv = ctx->nv, nx = ctx->nx, H = ctx->H;
   const size_t bytes = (size_t)nv * nx * H * ctx->nslabs * sizeof(double);
   if (!ctx->out_stream) {

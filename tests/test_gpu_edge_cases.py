@@ -257,3 +257,52 @@ def test_full_size_random_euler_every_seam():
         out = O.transport_step(bcfg, W0[rows], dt)
         assert np.array_equal(W1[[r % n for r in range(j0, j0 + 8)]], out[1:-1]), j0
     del W0, W1
+
+
+# ------------------------------------------------- FAST kernel range fallback
+@pytest.mark.parametrize("mode", [O.FIXED, O.ADAPTIVE])
+@pytest.mark.parametrize("flags", [0, fv2d.FLAG_GRAPH])
+def test_fast_division_out_of_range_cells_rerun_exactly(mode, flags, capfd, monkeypatch):
+    """The Euler pair kernel divides and takes square roots branch-free (the
+    compiler's fast paths, same bits inside their range).  Admissible cells
+    whose operands fall outside that range -- a subnormal density (1/rho still
+    finite) and a subnormal gamma*p/rho -- make the step re-run with the exact
+    kernel: state and dt log stay bitwise the oracle's, and the library reports
+    the re-run (FV2D_DEBUG_FAST)."""
+    monkeypatch.setenv("FV2D_DEBUG_FAST", "1")
+    nx, ny = 70, 44
+    cfg = O.Config(nx=nx, ny=ny, system=O.EULER, param=(G,))
+    W0 = inputs.euler_random(nx, ny, seed=11).copy()
+    W0[5, 7] = (1e-308, 0.0, 0.0, 1e-308)      # rho subnormal: 1/rho = 1e308, c = sqrt(0.56)
+    W0[30, 40] = (1.0, 0.0, 0.0, 1e-310)       # gamma*p/rho subnormal
+    value = 0.45 if mode == O.ADAPTIVE else 0.5 * 0.45 * (1.0 / nx) / O.smax(cfg, W0)[0]
+    ref = O.run(cfg, W0, 6, mode, value)
+    assert ref.status == 0
+    with solver_for(cfg, flags=flags) as s:
+        s.set_state(W0)
+        log = s.step_adaptive(value, 6) if mode == O.ADAPTIVE else s.step(value, 6)
+        W = s.get_state()
+    assert np.array_equal(W, ref.W)
+    if mode == O.ADAPTIVE:
+        assert np.array_equal(log, ref.dt_log)
+    assert "fast-path recovery" in capfd.readouterr().err
+
+
+def test_fast_division_genuine_error_still_reported():
+    """A non-admissible cell (p < 0) in a FAST step is re-run exactly and then
+    reported as the oracle reports it: E_NONFINITE at the same step, W^k kept."""
+    nx, ny = 64, 40
+    cfg = O.Config(nx=nx, ny=ny, system=O.EULER, param=(G,))
+    W0 = inputs.euler_random(nx, ny, seed=12).copy()
+    W0[10, 20, 3] = 0.0                          # E = 0 -> p < 0
+    dt = 1e-4
+    ref = O.run(cfg, W0, 3, O.FIXED, dt, raise_on_error=False)
+    assert ref.status == O.E_NONFINITE
+    with solver_for(cfg) as s:
+        s.set_state(W0)
+        s.step(dt, 3)
+        with pytest.raises(fv2d.FV2DError) as e:
+            s.synchronize()
+        assert e.value.code == fv2d.E_NONFINITE and e.value.step == ref.steps_done
+        assert e.value.cell == ref.err_cell
+        assert np.array_equal(s.get_state(raise_on_error=False), ref.W)

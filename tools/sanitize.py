@@ -69,4 +69,14 @@ with fv2d.Solver(256, 160, fv2d.EULER, param=(1.4,)) as s:
     s.step_host(pin, pin, dt, 2)
     assert np.all(np.isfinite(pin.array))
     pin.free()
+# FAST pair kernel: a subnormal density makes the library re-run the steps with
+# the exact kernel (recover_fast)
+W = inputs.euler_random(96, 64, seed=13).copy()
+W[5, 7] = (1e-308, 0.0, 0.0, 1e-308)
+with fv2d.Solver(96, 64, fv2d.EULER, param=(1.4,)) as s:
+    s.set_state(W)
+    s.step_adaptive(0.45, 3)
+    dt, _ = s.compute_dt(0.4)
+    s.step(dt, 2)
+    assert np.all(np.isfinite(s.get_state()))
 print("sanitize cases ok")
