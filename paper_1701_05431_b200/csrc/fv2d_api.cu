@@ -502,6 +502,12 @@ void launch_pair_x(const fv2d_ctx* ctx, const StepArgs& a, dim3 grid) {
       launch_pair_1<Sys, D, XM, true, true>(ctx, a, grid);
       return;
     }
+#if FV2D_FAST_FIXED
+    if (a.fast) {
+      launch_pair_1<Sys, D, XM, false, true>(ctx, a, grid);
+      return;
+    }
+#endif
   }
   if (a.adaptive) launch_pair_1<Sys, D, XM, true>(ctx, a, grid);
   else launch_pair_1<Sys, D, XM, false>(ctx, a, grid);
@@ -1581,7 +1587,7 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
   }
   const bool split = ctx->cfg.system == FV2D_SPRAY;
   const bool use_graph = (ctx->cfg.flags & FV2D_FLAG_GRAPH) && !ctx->use_nccl && !ctx->peer;
-  const bool fast = ctx->fast_ok && adaptive && !exact && !ctx->force_exact && !ctx->snap_used;
+  const bool fast = ctx->fast_ok && (adaptive || FV2D_FAST_FIXED) && !exact && !ctx->force_exact && !ctx->snap_used;
   for (int32_t k = 0; k < nsteps; ++k) {
     const int p = cur_parity(ctx);
     if (ctx->snap_parity == 1 - p) {  // this step writes the buffer a snapshot is reading

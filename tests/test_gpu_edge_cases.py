@@ -263,8 +263,8 @@ def test_full_size_random_euler_every_seam():
 @pytest.mark.parametrize("mode", [O.FIXED, O.ADAPTIVE])
 @pytest.mark.parametrize("flags", [0, fv2d.FLAG_GRAPH])
 def test_fast_division_out_of_range_cells_rerun_exactly(mode, flags, capfd, monkeypatch):
-    """The Euler pair kernel divides and takes square roots branch-free (the
-    compiler's fast paths, same bits inside their range).  Admissible cells
+    """The adaptive-dt Euler pair kernel divides and takes square roots
+    branch-free (the compiler's fast paths, same bits inside their range).  Admissible cells
     whose operands fall outside that range -- a subnormal density (1/rho still
     finite) and a subnormal gamma*p/rho -- make the step re-run with the exact
     kernel: state and dt log stay bitwise the oracle's, and the library reports
@@ -283,9 +283,9 @@ def test_fast_division_out_of_range_cells_rerun_exactly(mode, flags, capfd, monk
         log = s.step_adaptive(value, 6) if mode == O.ADAPTIVE else s.step(value, 6)
         W = s.get_state()
     assert np.array_equal(W, ref.W)
-    if mode == O.ADAPTIVE:
+    if mode == O.ADAPTIVE:  # (fixed dt runs the exact kernel: nothing to re-run)
         assert np.array_equal(log, ref.dt_log)
-    assert "fast-path recovery" in capfd.readouterr().err
+        assert "fast-path recovery" in capfd.readouterr().err
 
 
 def test_fast_division_genuine_error_still_reported():
