@@ -1,0 +1,5 @@
+set -u
+mkdir -p gpurun_out
+(timeout 900 python -m pytest tests -m gpu -x -q -k "spray or source or recon or edge or smoke" > gpurun_out/s3v_pytest.txt 2>&1; echo "exit $?" >> gpurun_out/s3v_pytest.txt)
+python tools/variants.py run nopreuse preuse nopreuse preuse --workload c4_spray_4096 --steps 200 > gpurun_out/s3v_c4.jsonl 2>&1
+echo done
