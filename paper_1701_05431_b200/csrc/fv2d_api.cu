@@ -1614,7 +1614,14 @@ static fv2d_status launch_steps(fv2d_ctx* ctx, int adaptive, double dt, double c
       st = issue_step(ctx, p, adaptive, dt, cfl, e1, fast);
       if (st) return st;
     }
-    if (ctx->fast_ok) ctx->journal.push_back({adaptive, dt, cfl, fast});
+    if (ctx->fast_ok) {
+      ctx->journal.push_back({adaptive, dt, cfl, fast});
+      if (ctx->journal.size() >= (1u << 16)) {  // bound the journal: settle it (one sync per 65536 steps)
+        unsigned long long s1;
+        st = read_status(ctx, &s1);
+        if (st) return st;
+      }
+    }
     if (split) ctx->lam_hist = std::min(3, ctx->lam_hist + 1);  // the source pass wrote lambda_{n+1}
     ctx->steps += 1;
   }
