@@ -306,3 +306,42 @@ def test_fast_division_genuine_error_still_reported():
         assert e.value.code == fv2d.E_NONFINITE and e.value.step == ref.steps_done
         assert e.value.cell == ref.err_cell
         assert np.array_equal(s.get_state(raise_on_error=False), ref.W)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fast_division_recovery_randomized(seed):
+    """Random Euler meshes, boundary conditions, slab counts, tiles and graph
+    mode with 1-3 admissible cells whose operands leave the branch-free range
+    (subnormal rho or subnormal gamma*p/rho), adaptive dt mixed with fixed-dt
+    runs: state and dt logs bitwise the oracle's."""
+    rng = np.random.default_rng(500 + seed)
+    nslabs = int(rng.choice([1, 1, 2]))
+    ny = int(rng.integers(4, 40)) * nslabs
+    nx = int(rng.integers(5, 200))
+    bcs = [O.BC_PERIODIC, O.BC_WALL, O.BC_DIRICHLET]
+    cfg = O.Config(nx=nx, ny=ny, system=O.EULER, param=(G,), bc_x=int(rng.choice(bcs)), bc_y=int(rng.choice(bcs)),
+                   dirichlet=(1.0, 0.1, -0.2, 2.6))
+    W0 = inputs.euler_random(nx, ny, seed=seed + 40).copy()
+    for _ in range(int(rng.integers(1, 4))):
+        j, i = int(rng.integers(0, ny)), int(rng.integers(0, nx))
+        W0[j, i] = (1e-308, 0.0, 0.0, 1e-308) if rng.random() < 0.5 else (1.0, 0.0, 0.0, 1e-310)
+    flags = int(rng.choice([0, fv2d.FLAG_GRAPH]))
+    tiles = (1, 1) if rng.random() < 0.6 or nx < 8 else (2, 2)
+    n1, n2 = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    C = 0.4
+    ref1 = O.run(cfg, W0, n1, O.ADAPTIVE, C, raise_on_error=False)
+    if ref1.status != O.OK:
+        pytest.skip(f"oracle status {ref1.status}")
+    dt = 0.5 * C * min(cfg.x1 - cfg.x0, cfg.y1 - cfg.y0) / max(nx, ny) / O.smax(cfg, ref1.W)[0]
+    ref2 = O.run(cfg, ref1.W, n2, O.FIXED, dt, raise_on_error=False)
+    ref3 = O.run(cfg, ref2.W, n1, O.ADAPTIVE, C, raise_on_error=False)
+    if ref2.status != O.OK or ref3.status != O.OK:
+        pytest.skip("oracle status")
+    with solver_for(cfg, nslabs=nslabs, flags=flags, tiles=tiles) as s:
+        s.set_state(W0)
+        l1 = s.step_adaptive(C, n1)
+        s.step(dt, n2)
+        l3 = s.step_adaptive(C, n1)
+        W = s.get_state()
+    assert np.array_equal(l1, ref1.dt_log) and np.array_equal(l3, ref3.dt_log)
+    assert np.array_equal(W, ref3.W)
